@@ -1,0 +1,139 @@
+/*
+ * robench_b200 — C ABI of the B200-native batched test-function evaluator.
+ *
+ * Drop-in boundary for the reference's evaluation path:
+ *   reference (Python rendition)            this ABI
+ *   engine.initialize      engine.py:225-228  rb_initialize
+ *   Engine.evaluate        engine.py:174-214  rb_func_evaluate   (device ptrs, fp64)
+ *   Engine.evaluate(...,"single")  :216-217   rb_func_evaluatef  (device ptrs, fp32)
+ *   (host-memory wrappers)                    rb_h_func_evaluate / rb_h_func_evaluatef
+ *   Engine.dispose         engine.py:219-222  rb_dispose
+ * The C names are the paper's own host API (initialize,
+ * func_evaluate, func_evaluatef, h_func_evaluate, h_func_evaluatef, dispose),
+ * prefixed rb_.  Values include the suite bias of +100 (engine.py:209).
+ *
+ * Plain C types only: pointers, sizes, status codes.  The instance pack is
+ * built on the host (paper_1407_7737_b200/pack.py) and copied to the device
+ * once in rb_initialize; the engine never retains caller pointers.
+ */
+#ifndef ROBENCH_B200_H
+#define ROBENCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes; 1:1 with the reference's exceptions (errors.py:4-52) */
+typedef int32_t rb_status;
+#define RB_OK                    0
+#define RB_E_UNKNOWN_FUNCTION    1  /* UnknownFunction   (catalog.py:224-229) */
+#define RB_E_DISABLED_FUNCTION   2  /* DisabledFunction  (engine.py:186-189)  */
+#define RB_E_BATCH_TOO_LARGE     3  /* BatchTooLarge     (engine.py:190-193)  */
+#define RB_E_DIMENSION_MISMATCH  4  /* DimensionMismatch (engine.py:194-195)  */
+#define RB_E_NON_FINITE_INPUT    5  /* NonFiniteInput    (engine.py:202-203, kernels.py:45-49) */
+#define RB_E_USE_AFTER_DISPOSE   6  /* UseAfterDispose   (engine.py:180-181)  */
+#define RB_E_INVALID_ARGUMENT    7  /* ValueError / malformed pack            */
+#define RB_E_UNSUPPORTED         8  /* configuration outside the built kernels */
+#define RB_E_CUDA                9  /* CUDA runtime failure                    */
+
+/* ---- instance pack ---------------------------------------------------- */
+/* Categories (catalog.py:25-29); RB_DISABLED marks ids switched off at
+ * dim < 10 (engine.py:148-154). */
+#define RB_DISABLED    (-1)
+#define RB_BASIC        0
+#define RB_HYBRID       1
+#define RB_COMPOSITION  2
+
+/* One diagonal block of a rotation: the block-diagonal-in-permuted-basis R
+ * of transforms.py:110-128 (3 groups), or a whole hybrid chunk rotation
+ * (transforms.py:137-140, 1 group).  Columns are stored in "q-order": sorted
+ * by the NumPy pairwise-sum accumulator slot they fall in (slot = column % 8
+ * below the last multiple of 8, then the ordered tail), ascending inside a
+ * slot, so exact-order single precision can replay NumPy's rounding
+ * (SURVEY.md Appendix A).  The segment length must be <= 128 for that. */
+typedef struct rb_group {
+  int32_t m;        /* block size */
+  int32_t qb[10];   /* slot s spans q in [qb[s], qb[s+1]) for s < 8; tail [qb[8], qb[9]); qb[9] == m */
+  int32_t col;      /* index[col + q]: input position (into the segment vector v) of the q-th column */
+  int32_t row;      /* index[row + r]: output position (into z) of block row r */
+  int32_t mat;      /* values[mat + q*m + r] = block[r][column of q] */
+} rb_group;
+
+/* One kernel application: v = scale*((x - o)[src..]) + pre; z = R v + post;
+ * value = K(z)  (engine.py:96-104, hybrid.py:108-114, composition.py:147-154). */
+typedef struct rb_segment {
+  int32_t kernel;    /* 0..20 in catalog.KERNEL_NAMES order */
+  int32_t d;         /* kernel length: dim, or the hybrid chunk size */
+  int32_t src;       /* offset of this chunk inside the member's split permutation (0 for basic) */
+  int32_t n_groups;  /* 0 = not rotated (ids 10, 15) */
+  int32_t group0;    /* first rb_group */
+  int32_t ctab;      /* values[ctab ...]: per-(kernel, d) constants computed by NumPy in the pack dtype */
+  double scale, pre, post;
+} rb_segment;
+
+/* A basic function, a hybrid, or one composition member (composition.py:25-40). */
+typedef struct rb_member {
+  int32_t n_segments;
+  int32_t segment0;
+  int32_t shift;     /* values[shift + j]: optimum o (dim) */
+  int32_t perm;      /* index[perm + t]: hybrid split permutation (dim), or -1 */
+  double sigma, height, bias;  /* composition blend (composition.py:114-166); unused otherwise */
+} rb_member;
+
+typedef struct rb_function {
+  int32_t category;  /* RB_DISABLED / RB_BASIC / RB_HYBRID / RB_COMPOSITION */
+  int32_t n_members;
+  int32_t member0;
+  int32_t reserved;
+} rb_function;
+
+typedef struct rb_pack {
+  int32_t dim;
+  int32_t n_functions;                 /* 37 */
+  const rb_function* functions;
+  int32_t n_members;   const rb_member*  members;
+  int32_t n_segments;  const rb_segment* segments;
+  int32_t n_groups;    const rb_group*   groups;
+  int64_t n_index;     const int32_t*    index;
+  int64_t n_values;                    /* length of both value tables */
+  const double* values_f64;            /* shifts, rotations, constants in float64 */
+  const float*  values_f32;            /* the same, cast / recomputed in float32 */
+} rb_pack;
+
+typedef struct rb_engine rb_engine;
+
+/* ---- lifecycle -------------------------------------------------------- */
+rb_status rb_initialize(const rb_pack* pack, int64_t max_concurrency, int32_t device,
+                        rb_engine** out);
+rb_status rb_dispose(rb_engine** engine);          /* idempotent; *engine = NULL */
+
+/* ---- evaluation: f[i] = F_fn(x[i, :]) + 100 ---------------------------- */
+/* Device pointers, stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ * default).  x is row-major n x dim.  Synchronises on `stream` only to read
+ * the non-finite flag; on RB_E_NON_FINITE_INPUT the contents of f are
+ * unspecified (the reference returns no values). */
+rb_status rb_func_evaluate (rb_engine* e, int32_t fn_id, const double* x, int64_t n,
+                            double* f, void* stream);
+rb_status rb_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n,
+                            float* f, void* stream);
+/* Host-memory wrappers (paper: h_func_evaluate / h_func_evaluatef). */
+rb_status rb_h_func_evaluate (rb_engine* e, int32_t fn_id, const double* x, int64_t n,
+                              double* f);
+rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n,
+                              float* f);
+
+/* ---- introspection ---------------------------------------------------- */
+const char* rb_last_error(void);                   /* thread-local message */
+int32_t rb_abi_version(void);
+/* sizeof of rb_group, rb_segment, rb_member, rb_function, rb_pack (host
+ * layout check for FFI bindings). */
+void rb_struct_sizes(int64_t out[5]);
+/* Number of kernel launches issued by this process so far (bench evidence). */
+int64_t rb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROBENCH_B200_H */

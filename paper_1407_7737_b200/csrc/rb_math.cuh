@@ -1,0 +1,113 @@
+// Precision-generic math and the NumPy-order reductions used by every kernel.
+//
+// Build flags (see build.py): -fmad=false so no a*b+c in this code is ever
+// contracted into an FMA — NumPy rounds every product —
+// and IEEE division / square root (no fast-math).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RB_FULL 0xffffffffu
+
+namespace rb {
+
+// ---------------------------------------------------------------- math
+// float64: CUDA's double libm (<= 2 ulp).  float32: evaluated in double and
+// rounded once, i.e. (almost always) the correctly rounded float result;
+// NumPy's float32 SIMD transcendentals are within ~1-2 ulp of that
+// (measured on the box).
+template <class T> struct M;
+
+template <> struct M<double> {
+  static __device__ __forceinline__ double cos(double x) { return ::cos(x); }
+  static __device__ __forceinline__ double sin(double x) { return ::sin(x); }
+  static __device__ __forceinline__ double exp(double x) { return ::exp(x); }
+  static __device__ __forceinline__ double log(double x) { return ::log(x); }
+  static __device__ __forceinline__ double expm1(double x) { return ::expm1(x); }
+  static __device__ __forceinline__ double pow(double x, double y) { return ::pow(x, y); }
+  static __device__ __forceinline__ double sqrt(double x) { return ::sqrt(x); }
+  static __device__ __forceinline__ double floor(double x) { return ::floor(x); }
+  static __device__ __forceinline__ double fabs(double x) { return ::fabs(x); }
+  static __device__ __forceinline__ double fmod(double x, double y) { return ::fmod(x, y); }
+  static __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+};
+
+template <> struct M<float> {
+  static __device__ __forceinline__ float cos(float x) { return (float)::cos((double)x); }
+  static __device__ __forceinline__ float sin(float x) { return (float)::sin((double)x); }
+  static __device__ __forceinline__ float exp(float x) { return (float)::exp((double)x); }
+  static __device__ __forceinline__ float log(float x) { return (float)::log((double)x); }
+  static __device__ __forceinline__ float expm1(float x) { return (float)::expm1((double)x); }
+  static __device__ __forceinline__ float pow(float x, float y) {
+    return (float)::pow((double)x, (double)y);
+  }
+  static __device__ __forceinline__ float sqrt(float x) { return ::sqrtf(x); }
+  static __device__ __forceinline__ float floor(float x) { return ::floorf(x); }
+  static __device__ __forceinline__ float fabs(float x) { return ::fabsf(x); }
+  static __device__ __forceinline__ float fmod(float x, float y) { return ::fmodf(x, y); }
+  static __device__ __forceinline__ bool finite(float x) { return isfinite(x); }
+};
+
+// Python-double constant as NumPy casts it into the working dtype (NEP 50:
+// the weak Python float is rounded once to T).
+template <class T> __device__ __forceinline__ T C(double v) { return static_cast<T>(v); }
+
+// ------------------------------------------------------- 8-lane pairwise sum
+// A point is owned by 8 consecutive lanes (l8 = lane & 7).  pw8 returns, in
+// all 8 lanes, NumPy's float sum of f(lo), ..., f(lo+n-1) with NumPy's exact
+// association (umath pairwise sum):
+//   n < 8     : ((0 + a0) + a1) + ...
+//   8..128    : 8 strided accumulators r_k over a[k], a[k+8], ... below the
+//               last multiple of 8, combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//               then the tail added in order
+//   > 128     : pw(first m) + pw(rest), m = n/2 rounded down to a multiple of 8
+// Lane k is accumulator r_k; the combine is the xor butterfly 1, 2, 4.
+// f is called once per element, by the lane that owns it.
+template <class T, class F>
+__device__ __forceinline__ T pw8_leaf(int lo, int n, F& f, int l8) {
+  T r = T(0);
+  const int main_len = n < 8 ? 0 : n - (n & 7);
+  if (main_len) {
+    for (int i = l8; i < main_len; i += 8) r = r + f(lo + i);
+    r = r + __shfl_xor_sync(RB_FULL, r, 1, 8);
+    r = r + __shfl_xor_sync(RB_FULL, r, 2, 8);
+    r = r + __shfl_xor_sync(RB_FULL, r, 4, 8);
+  }
+  const int tail = n - main_len;
+  if (tail) {
+    const T v = (l8 < tail) ? f(lo + main_len + l8) : T(0);
+    for (int k = 0; k < tail; ++k) r = r + __shfl_sync(RB_FULL, v, k, 8);
+  }
+  return r;
+}
+
+template <class T, class F>
+__device__ T pw8_tree(int lo, int n, F& f, int l8) {
+  if (n <= 128) return pw8_leaf<T>(lo, n, f, l8);
+  int m = n >> 1;
+  m -= m & 7;
+  const T a = pw8_tree<T>(lo, m, f, l8);
+  const T b = pw8_tree<T>(lo + m, n - m, f, l8);
+  return a + b;
+}
+
+template <class T, class F>
+__device__ __forceinline__ T pw8(int lo, int n, F&& f, int l8) {
+  if (n <= 128) return pw8_leaf<T>(lo, n, f, l8);
+  return pw8_tree<T>(lo, n, f, l8);
+}
+
+// Sequential product over i = 0..n-1 of f(i) (np.prod is a plain left fold,
+// kernels.py:112); lane l8 evaluates the i = l8 (mod 8) factors.
+template <class T, class F>
+__device__ __forceinline__ T prod8(int n, F&& f, int l8) {
+  T p = T(1);
+  for (int base = 0; base < n; base += 8) {
+    const int cnt = min(8, n - base);
+    const T v = (l8 < cnt) ? f(base + l8) : T(1);
+    for (int k = 0; k < cnt; ++k) p = p * __shfl_sync(RB_FULL, v, k, 8);
+  }
+  return p;
+}
+
+}  // namespace rb

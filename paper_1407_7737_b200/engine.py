@@ -1,0 +1,192 @@
+"""Drop-in engine: the reference's ``initialize / Engine.evaluate /
+evaluate_single_precision / dispose`` API (engine.py:34-228) over the
+native C ABI.
+
+Same types (EngineConfig, PointBatch, EvalResult), same validation order and
+exception classes (engine.py:180-203), same values (+100 bias, the batch
+dtype).  Differences, all additive:
+
+* ``EngineConfig.device`` selects the GPU; ``threads`` is accepted and
+  ignored (the per-point parallelism lives on the device).
+* ``evaluate`` also accepts a CUDA ``torch.Tensor`` (N x D); the points then
+  never leave the device and ``EvalResult.values`` is a CUDA tensor.  NumPy
+  input goes through the host wrappers (rb_h_func_evaluate[f]) and returns
+  NumPy, exactly like the reference.
+
+Every evaluation runs on the GPU; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, catalog
+from .errors import (BatchTooLarge, DimensionMismatch, DimensionTooSmall, DisabledFunction,
+                     UseAfterDispose)
+from .pack import Pack
+
+_DTYPES = {"double": np.float64, "single": np.float32}
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch") and hasattr(x, "is_cuda")
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """engine.py:34-52, plus ``device``."""
+
+    dim: int
+    max_concurrency: int = 50
+    seed: int = 0
+    precision: str = "double"
+    threads: int = 1
+    device: int = 0
+
+    def __post_init__(self):
+        if self.dim < catalog.MIN_DIMENSION:
+            raise DimensionTooSmall(f"dim must be >= {catalog.MIN_DIMENSION}, got {self.dim}")
+        if self.max_concurrency < 1:
+            raise ValueError("max_concurrency must be >= 1")
+        if self.seed < 0:
+            raise ValueError("seed must be a non-negative integer")
+        if self.precision not in _DTYPES:
+            raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+
+
+@dataclass(frozen=True)
+class PointBatch:
+    """N x D points (engine.py:55-77); NumPy array or CUDA torch tensor."""
+
+    data: object
+
+    def __post_init__(self):
+        arr = self.data if _is_torch(self.data) else np.asarray(self.data)
+        if arr.ndim != 2 or arr.shape[0] < 1:
+            raise ValueError("batch data must be a non-empty 2-D array")
+        object.__setattr__(self, "data", arr)
+
+    @property
+    def count(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def dim(self) -> int:
+        return int(self.data.shape[1])
+
+    @property
+    def precision(self) -> str:
+        dt = self.data.dtype
+        if _is_torch(self.data):
+            import torch
+            return "single" if dt == torch.float32 else "double"
+        return "single" if dt == np.float32 else "double"
+
+
+@dataclass(frozen=True)
+class EvalResult:
+    values: object
+
+
+class Engine:
+    """All 37 instances of one (dim, seed), resident on one GPU."""
+
+    def __init__(self, config: EngineConfig):
+        self.config = config
+        self._disposed = False
+        dim = config.dim
+        if dim >= catalog.MIN_CONSTRUCTED_DIMENSION:
+            self._disabled = frozenset()
+        else:                                               # engine.py:148-154
+            self._disabled = frozenset(r.fn_id for r in catalog.FUNCTIONS
+                                       if r.category in (catalog.HYBRID, catalog.COMPOSITION))
+        lib = _lib.load()
+        self._pack = Pack(dim, config.seed, self._disabled)
+        handle = ctypes.c_void_p()
+        _lib.check(lib.rb_initialize(ctypes.byref(_lib.make_pack(self._pack)),
+                                     int(config.max_concurrency), int(config.device),
+                                     ctypes.byref(handle)))
+        self._handle = handle
+
+    @property
+    def dim(self) -> int:
+        return self.config.dim
+
+    @property
+    def disabled_ids(self) -> frozenset:
+        return self._disabled
+
+    @property
+    def enabled_ids(self) -> tuple:
+        return tuple(fn for fn in range(catalog.FUNCTION_COUNT) if fn not in self._disabled)
+
+    def evaluate(self, fn_id: int, batch, precision: str | None = None) -> EvalResult:
+        """Score every point of ``batch`` against ``fn_id`` (engine.py:174-214)."""
+        if self._disposed:
+            raise UseAfterDispose("engine was disposed")
+        if not isinstance(batch, PointBatch):
+            batch = PointBatch(batch)
+        catalog.lookup(fn_id)
+        fn_id = int(fn_id)
+        if fn_id in self._disabled:
+            raise DisabledFunction(
+                f"function {fn_id} needs dimension >= {catalog.MIN_CONSTRUCTED_DIMENSION}")
+        if batch.count > self.config.max_concurrency:
+            raise BatchTooLarge(f"batch of {batch.count} exceeds "
+                                f"max_concurrency={self.config.max_concurrency}")
+        if batch.dim != self.config.dim:
+            raise DimensionMismatch(f"batch dim {batch.dim} != engine dim {self.config.dim}")
+        precision = precision or self.config.precision
+        if precision not in _DTYPES:
+            raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
+        if _is_torch(batch.data):
+            return EvalResult(self._evaluate_device(fn_id, batch.data, precision))
+        return EvalResult(self._evaluate_host(fn_id, batch.data, precision))
+
+    def evaluate_single_precision(self, fn_id: int, batch) -> EvalResult:
+        return self.evaluate(fn_id, batch, precision="single")
+
+    def dispose(self) -> None:
+        """Free the device pack; a second dispose is a no-op (engine.py:219-222)."""
+        if not self._disposed:
+            _lib.check(_lib.load().rb_dispose(ctypes.byref(self._handle)))
+            self._pack = None
+        self._disposed = True
+
+    def __del__(self):
+        try:
+            self.dispose()
+        except Exception:
+            pass
+
+    # -- paths
+    def _evaluate_host(self, fn_id, data, precision):
+        dt = _DTYPES[precision]
+        pts = np.ascontiguousarray(data, dtype=dt)          # engine.py:201
+        out = np.empty(pts.shape[0], dtype=dt)
+        call = _lib.load().rb_h_func_evaluate if dt is np.float64 else _lib.load().rb_h_func_evaluatef
+        _lib.check(call(self._handle, fn_id, _lib.ptr(pts), pts.shape[0], _lib.ptr(out)))
+        return out
+
+    def _evaluate_device(self, fn_id, data, precision):
+        import torch
+        if not data.is_cuda or data.device.index != self.config.device:
+            raise ValueError(f"tensor must live on cuda:{self.config.device}")
+        dt = torch.float64 if precision == "double" else torch.float32
+        pts = data.to(dt).contiguous()
+        out = torch.empty(pts.shape[0], dtype=dt, device=pts.device)
+        stream = torch.cuda.current_stream(pts.device).cuda_stream
+        call = _lib.load().rb_func_evaluate if dt == torch.float64 else _lib.load().rb_func_evaluatef
+        _lib.check(call(self._handle, fn_id, pts.data_ptr(), pts.shape[0], out.data_ptr(), stream))
+        return out
+
+
+def initialize(config: EngineConfig) -> Engine:
+    """Build every instance on the host, upload the pack, return the engine
+    (engine.py:225-228)."""
+    return Engine(config)

@@ -1,0 +1,215 @@
+"""Flatten the host-built instances of one (dim, seed) into the device pack.
+
+The pack is the ``rb_pack`` of include/robench_b200.h: four descriptor
+tables (functions, members, segments, groups), one int32 index table and two
+value tables of equal length (float64 and float32).  rb_initialize copies it
+to the device once; evaluation never touches the host copy again.
+
+Layout decisions:
+
+* Rotations are stored per diagonal block, never dense: R is block-diagonal
+  in a permuted basis (transforms.py:110-128), so only sum(n_b^2) of the
+  D^2 entries exist (3 334 of 10 000 at D=100).
+* Block columns are stored in *q-order*: grouped by the accumulator slot the
+  column occupies in NumPy's pairwise row sum (slot = column % 8 below the
+  last multiple of 8, then the sequential tail), ascending within a slot.
+  The exact-order float32 rotate walks q-order and reproduces the rounding of
+  ``(R * v).sum(axis=1)`` (transforms.py:42-48) bit for bit; structural zeros
+  of the dense row are exact no-ops and are skipped.
+* Per-(kernel, d) constant arrays that the reference builds with NumPy in the
+  working dtype (elliptic weights kernels.py:66-67, powers exponents :83,
+  Weierstrass series :100-106, Katsuura scalars :177-184) are computed here
+  with the very same NumPy expressions in each dtype, so both sides see the
+  same bits on the machine that runs them.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import catalog, instances
+
+GROUP_DT = np.dtype([("m", "<i4"), ("qb", "<i4", (10,)), ("col", "<i4"),
+                     ("row", "<i4"), ("mat", "<i4")])
+SEGMENT_DT = np.dtype({
+    "names": ["kernel", "d", "src", "n_groups", "group0", "ctab", "scale", "pre", "post"],
+    "formats": ["<i4"] * 6 + ["<f8"] * 3,
+    "offsets": [0, 4, 8, 12, 16, 20, 24, 32, 40], "itemsize": 48})
+MEMBER_DT = np.dtype({
+    "names": ["n_segments", "segment0", "shift", "perm", "sigma", "height", "bias"],
+    "formats": ["<i4"] * 4 + ["<f8"] * 3,
+    "offsets": [0, 4, 8, 12, 16, 24, 32], "itemsize": 40})
+FUNCTION_DT = np.dtype([("category", "<i4"), ("n_members", "<i4"), ("member0", "<i4"),
+                        ("reserved", "<i4")])
+
+CATEGORY = {catalog.UNIMODAL: 0, catalog.BASIC_MULTIMODAL: 0,
+            catalog.HYBRID: 1, catalog.COMPOSITION: 2}
+DISABLED = -1
+EXACT_ORDER_MAX = 128   # single-leaf pairwise sum; longer rows need the recursive tree
+
+
+def slot_of(pos: int, n: int) -> int:
+    """Accumulator slot of element ``pos`` in NumPy's pairwise sum of a
+    contiguous length-n row: 0..7, or 8 for the tail."""
+    main = 0 if n < 8 else n - n % 8
+    return pos % 8 if pos < main else 8
+
+
+def kernel_constants(kernel: str, d: int, dt) -> np.ndarray:
+    """Constant table of one kernel at length d, computed with the
+    reference's own NumPy expressions in dtype ``dt``."""
+    if kernel == "elliptic":                                   # kernels.py:66-67
+        e = np.arange(d, dtype=dt) / max(d - 1, 1)
+        return np.asarray(1.0e6**e, dtype=dt)
+    if kernel == "powers":                                     # kernels.py:83
+        return np.asarray(2.0 + 4.0 * np.arange(d, dtype=dt) / max(d - 1, 1), dtype=dt)
+    if kernel == "weierstrass":                                # kernels.py:100-106
+        k = np.arange(21, dtype=dt)
+        ak, bk = 0.5**k, 3.0**k
+        arg = 2.0 * np.pi * bk        # left operand of "* (z[:, None] + 0.5)"
+        base = np.sum(ak * np.cos(np.pi * bk))
+        return np.concatenate([ak, arg, np.asarray([d * base], dtype=dt)]).astype(dt)
+    if kernel == "katsuura":                                   # kernels.py:183-184
+        return np.asarray([10.0 / d**1.2, 10.0 / (d * d)], dtype=dt)
+    return np.zeros(0, dtype=dt)
+
+
+class _Builder:
+    def __init__(self, dim: int):
+        self.dim = dim
+        self.functions = np.zeros(catalog.FUNCTION_COUNT, dtype=FUNCTION_DT)
+        self.members, self.segments, self.groups = [], [], []
+        self.index: list[np.ndarray] = []
+        self.n_index = 0
+        self.v64: list[np.ndarray] = []
+        self.v32: list[np.ndarray] = []
+        self.n_values = 0
+        self.max_exact_len = 0   # longest rotated segment (exact-order fp32 bound)
+        self.max_q = 0           # widest per-segment sum of 4-padded group sizes
+        self.max_d = 0
+
+    # -- tables
+    def values(self, a64, a32=None) -> int:
+        a64 = np.ascontiguousarray(a64, dtype=np.float64).ravel()
+        a32 = (a64.astype(np.float32) if a32 is None
+               else np.ascontiguousarray(a32, dtype=np.float32).ravel())
+        assert a64.shape == a32.shape
+        off = self.n_values
+        self.v64.append(a64)
+        self.v32.append(a32)
+        self.n_values += a64.size
+        return off
+
+    def ints(self, a) -> int:
+        a = np.ascontiguousarray(a, dtype=np.int32).ravel()
+        off = self.n_index
+        self.index.append(a)
+        self.n_index += a.size
+        return off
+
+    # -- descriptors
+    def group(self, block: np.ndarray, cols, rows, n: int) -> int:
+        """One rotation block acting on positions ``cols`` of a length-n
+        segment vector and writing positions ``rows`` of z."""
+        m = block.shape[0]
+        cols = [int(c) for c in cols]
+        order = sorted(range(m), key=lambda k: (slot_of(cols[k], n), cols[k]))
+        slots = [slot_of(cols[k], n) for k in order]
+        qb = np.searchsorted(np.asarray(slots), np.arange(10), side="left").astype(np.int32)
+        qb[9] = m
+        mat = np.ascontiguousarray(block[:, order].T)          # mat[q, r] = block[r, order[q]]
+        rec = np.zeros((), dtype=GROUP_DT)
+        rec["m"] = m
+        rec["qb"] = qb
+        rec["col"] = self.ints([cols[k] for k in order])
+        rec["row"] = self.ints(rows)
+        rec["mat"] = self.values(mat)
+        self.groups.append(rec)
+        return len(self.groups) - 1
+
+    def segment(self, kernel: str, d: int, src: int, blocks) -> int:
+        """blocks: list of (block, cols, rows) or [] when not rotated."""
+        scale, pre, post = catalog.KERNEL_PIPELINE[kernel]
+        g0 = len(self.groups)
+        for blk, cols, rows in blocks:
+            self.group(blk, cols, rows, d)
+        if blocks:
+            self.max_exact_len = max(self.max_exact_len, d)
+            self.max_q = max(self.max_q, sum((b.shape[0] + 3) // 4 * 4 for b, _, _ in blocks))
+        self.max_d = max(self.max_d, d)
+        c64, c32 = kernel_constants(kernel, d, np.float64), kernel_constants(kernel, d, np.float32)
+        rec = np.zeros((), dtype=SEGMENT_DT)
+        rec["kernel"] = catalog.KERNEL_IDS[kernel]
+        rec["d"] = d
+        rec["src"] = src
+        rec["n_groups"] = len(blocks)
+        rec["group0"] = g0
+        rec["ctab"] = self.values(c64, c32) if c64.size else 0
+        rec["scale"], rec["pre"], rec["post"] = scale, pre, post
+        self.segments.append(rec)
+        return len(self.segments) - 1
+
+    def member(self, shift, segs: list[int], perm=None, sigma=0.0, height=0.0, bias=0.0) -> int:
+        rec = np.zeros((), dtype=MEMBER_DT)
+        rec["n_segments"] = len(segs)
+        rec["segment0"] = segs[0]
+        rec["shift"] = self.values(shift)
+        rec["perm"] = -1 if perm is None else self.ints(perm)
+        rec["sigma"], rec["height"], rec["bias"] = sigma, height, bias
+        self.members.append(rec)
+        return len(self.members) - 1
+
+    def rotated_segment(self, kernel: str, rot: instances.GroupedRotation) -> int:
+        return self.segment(kernel, self.dim, 0, [(blk, idx, idx) for idx, blk in rot.groups()])
+
+    def hybrid_segments(self, h: instances.HybridInstance) -> list[int]:
+        segs, off = [], 0
+        for name, n, mat in zip(h.kernels, h.sizes, h.chunk_rotations):
+            ar = np.arange(n)
+            segs.append(self.segment(name, n, off, [(mat, ar, ar)]))
+            off += n
+        return segs
+
+
+class Pack:
+    """Host copy of an ``rb_pack`` (numpy arrays kept alive for the FFI)."""
+
+    def __init__(self, dim: int, seed: int, disabled=frozenset()):
+        b = _Builder(dim)
+        for fn in range(catalog.FUNCTION_COUNT):
+            rec = b.functions[fn]
+            if fn in disabled:
+                rec["category"] = DISABLED
+                continue
+            inst = instances.build(fn, dim, seed)
+            row = catalog.lookup(fn)
+            rec["category"] = CATEGORY[row.category]
+            rec["member0"] = len(b.members)
+            if isinstance(inst, instances.BasicInstance):
+                if inst.rotation is None:
+                    seg = b.segment(inst.kernel, dim, 0, [])
+                else:
+                    seg = b.rotated_segment(inst.kernel, inst.rotation)
+                b.member(inst.shift, [seg])
+                rec["n_members"] = 1
+            elif isinstance(inst, instances.HybridInstance):
+                b.member(inst.shift, b.hybrid_segments(inst), perm=inst.split_perm)
+                rec["n_members"] = 1
+            else:
+                for k, m in enumerate(inst.members):
+                    blend = dict(sigma=inst.sigma[k], height=inst.heights[k], bias=inst.biases[k])
+                    if m.hybrid is not None:
+                        b.member(m.shift, b.hybrid_segments(m.hybrid), perm=m.hybrid.split_perm, **blend)
+                    else:
+                        b.member(m.shift, [b.rotated_segment(m.kernel, m.rotation)], **blend)
+                rec["n_members"] = len(inst.members)
+        self.dim, self.seed = dim, seed
+        self.functions = b.functions
+        self.members = np.array(b.members, dtype=MEMBER_DT) if b.members else np.zeros(0, MEMBER_DT)
+        self.segments = np.array(b.segments, dtype=SEGMENT_DT) if b.segments else np.zeros(0, SEGMENT_DT)
+        self.groups = np.array(b.groups, dtype=GROUP_DT) if b.groups else np.zeros(1, GROUP_DT)
+        self.index = np.concatenate(b.index) if b.index else np.zeros(1, np.int32)
+        self.values_f64 = np.concatenate(b.v64) if b.v64 else np.zeros(1)
+        self.values_f32 = np.concatenate(b.v32) if b.v32 else np.zeros(1, np.float32)
+        self.max_exact_len = b.max_exact_len
+        self.max_q, self.max_d = b.max_q, b.max_d
