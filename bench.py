@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the suite evaluation path (driver contract).
+
+Workload (BASELINE.json metric "function evals/sec at D=100 FP64/FP32";
+config 5 on one GPU): one *step* evaluates all 37 functions in float64 and
+in float32 on a synthetic population X ~ U[-100,100]^{N x 100}, N = 10^7
+(8 GB fp64 + 4 GB fp32, far larger than the 126 MB L2, so every launch
+streams X from HBM).  value = 37 * 2 * N * steps / time, whole job.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun): rows are sharded (dist.Shard, strong scaling: N fixed),
+each rank evaluates its rows and the fitness vector is all-gathered over
+NCCL inside the timed step; time = max over ranks.
+
+Keys beyond the base contract:
+  e2e           same metric through the public API with the population in
+                pinned host memory: per step one H2D copy of X, the fp32
+                cast, 74 evaluations, one D2H read of every fitness vector.
+  roofline      dominant (function, precision) launch: T_roof / T_measured,
+                T_roof = max(N*(D+1)*s / HBM, N*F / P_fp),
+                F = 2*nnz of the rotations applied; P_fp = measured DMMA fp64
+                (fp64) or exact-order FMUL+FADD (fp32) peak on this pool
+                (profiles/peaks_r01.json), HBM from MEASURED_PEAKS.json.
+  cpu_baseline  the reference path (CPU oracle port, per-point NumPy loop as
+                engine.py:205-209) timed on a bounded row sample on all host
+                cores, rank 0, N=1 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "function evals/sec at D=100 FP64/FP32 vs CPU ref; fraction of roofline"
+UNIT = "evals/s"
+PREC = ("double", "single")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--dim", type=int, default=100)
+    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--fns", default="all", help="comma list of ids (default: all 37)")
+    ap.add_argument("--precisions", default="double,single")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=32, help="rows per process per (fn, precision)")
+    ap.add_argument("--breakdown", default="", help="write per-(fn, precision) timings here")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+def load_json(path):
+    try:
+        return json.loads(Path(path).read_text())
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc = index, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def rotate_flops(pack, fn: int) -> int:
+    """F = 2 * nnz of every rotation one evaluation applies."""
+    rec = pack.functions[fn]
+    total = 0
+    for mi in range(rec["member0"], rec["member0"] + rec["n_members"]):
+        mem = pack.members[mi]
+        for si in range(mem["segment0"], mem["segment0"] + mem["n_segments"]):
+            seg = pack.segments[si]
+            for gi in range(seg["group0"], seg["group0"] + seg["n_groups"]):
+                total += 2 * int(pack.groups[gi]["m"]) ** 2
+    return total
+
+
+# ------------------------------------------------------------ CPU baseline
+def _cpu_worker(job):
+    dim, fns, precs, rows = job
+    sys.path.insert(0, str(ROOT))
+    from oracle.robench_oracle import Oracle
+    orc = Oracle(dim, 0)
+    for fn in fns:                      # build outside the timed loop (initialize)
+        for p in precs:
+            orc.evaluator(fn, p)
+    t0 = time.perf_counter()
+    n = 0
+    for fn in fns:
+        for p in precs:
+            orc.evaluate(fn, rows, p)
+            n += rows.shape[0]
+    return n, time.perf_counter() - t0
+
+
+def cpu_reference(dim, fns, precs, rows_per_proc, x_rows=None, procs=None):
+    """The reference's per-point path (oracle port, bit-identical to
+    robench) on every host core: P processes over disjoint row slices."""
+    import multiprocessing as mp
+    procs = procs or os.cpu_count() or 1
+    if x_rows is None:
+        rng = np.random.default_rng(1001)
+        x_rows = rng.uniform(-100.0, 100.0, (rows_per_proc * procs, dim))
+    jobs = [(dim, fns, precs, x_rows[i * rows_per_proc:(i + 1) * rows_per_proc])
+            for i in range(procs)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    evals = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": evals / wall, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": (f"{rows_per_proc * procs} rows x {len(fns)} fns x {len(precs)} precisions "
+                       f"at D={dim} ({procs} processes x {rows_per_proc} rows, per-point NumPy "
+                       f"loop = engine.py:205-209, oracle/robench_oracle.py)"),
+            "cpu_seconds": sum(r[1] for r in res)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    fns = list(range(37)) if args.fns == "all" else [int(f) for f in args.fns.split(",")]
+    precs = [p for p in args.precisions.split(",")]
+    for _ in range(max(args.warmup, 0)):
+        cpu_reference(args.dim, fns, precs, max(2, args.cpu_rows // 8))
+    vals = [cpu_reference(args.dim, fns, precs, args.cpu_rows) for _ in range(args.steps)]
+    cores = vals[0]["cores"]
+    value = statistics.median(v["value"] for v in vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * 37 * len(precs) * args.n / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64+f32", "data": "synthetic U[-100,100]^D",
+        "config": {"workload": f"suite-sweep D={args.dim} N={args.n} (37 fns x {len(precs)} precisions)",
+                   "dim": args.dim, "n": args.n, "fns": len(fns), "precisions": precs,
+                   "sample": vals[0]["sample"]},
+        "cpu_baseline": {k: vals[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1407_7737_b200 import EngineConfig, _lib, initialize
+    from paper_1407_7737_b200.dist import Shard, gather_fitness
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    D = args.dim
+    shard = Shard(rank, world, args.n)
+    fns_req = None if args.fns == "all" else [int(f) for f in args.fns.split(",")]
+    precs = [p for p in args.precisions.split(",")]
+    engine = initialize(EngineConfig(dim=D, max_concurrency=max(shard.count, 1), seed=0,
+                                     device=local))
+    fns = [f for f in engine.enabled_ids if fns_req is None or f in fns_req]
+    flops = {fn: rotate_flops(engine._pack, fn) for fn in fns}
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1001 + rank)
+    x64 = torch.rand((shard.count, D), dtype=torch.float64, device=dev, generator=gen)
+    x64.mul_(200.0).sub_(100.0)
+    x32 = x64.float()
+    xs = {"double": x64, "single": x32}
+    stream = torch.cuda.current_stream()
+
+    per = {}
+
+    def step(record):
+        for p in precs:
+            for fn in fns:
+                if record:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                local_f = engine.evaluate(fn, xs[p], p).values
+                if record:
+                    e1.record(stream)
+                    per.setdefault((fn, p), []).append((e0, e1))
+                gather_fitness(local_f, shard)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    evals = args.steps * len(fns) * len(precs) * args.n
+    value = evals / (ms / 1e3)
+
+    # per-(fn, precision) device time and roofline
+    peaks = load_json(ROOT / "MEASURED_PEAKS.json")
+    mypk = load_json(ROOT / "profiles" / "peaks_r01.json")
+    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    p_fp = {"double": float(mypk.get("dmma_m16n8k4_tflops", 36.9)) * 1e12,
+            "single": float(mypk.get("fmul_fadd_tflops", 65.5)) * 1e12}
+    rows = []
+    for (fn, p), evs in per.items():
+        t = sum(a.elapsed_time(b) for a, b in evs) / 1e3 / len(evs)
+        s = 8 if p == "double" else 4
+        t_hbm = shard.count * (D + 1) * s / hbm
+        t_fp = shard.count * flops[fn] / p_fp[p]
+        rows.append({"fn": fn, "precision": p, "seconds": t, "evals_per_s": shard.count / t,
+                     "t_roof_hbm": t_hbm, "t_roof_fp": t_fp, "frac": max(t_hbm, t_fp) / t,
+                     "rotate_flops_per_eval": flops[fn]})
+    rows.sort(key=lambda r: -r["seconds"])
+    dom = rows[0]
+    bound = "hbm" if dom["t_roof_hbm"] >= dom["t_roof_fp"] else "tensor"
+    if bound == "hbm":
+        achieved = shard.count * (D + 1) * (8 if dom["precision"] == "double" else 4) / dom["seconds"] / 1e9
+        peak, unit = hbm / 1e9, "GB/s"
+    else:
+        achieved = shard.count * flops[dom["fn"]] / dom["seconds"] / 1e12
+        peak, unit = p_fp[dom["precision"]] / 1e12, "TFLOP/s"
+    traffic = load_json(ROOT / "profiles" / "ncu_traffic_r01.json").get(
+        f"{dom['fn']}/{dom['precision']}")
+    roofline = {
+        "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+        "frac": achieved / peak, "traffic": traffic,
+        "kernel": f"rb::evaluate_kernel<{'double' if dom['precision'] == 'double' else 'float'}> "
+                  f"fn={dom['fn']}",
+        "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
+                        "profiles/peaks_r01.json (tools/peaks_microbench.cu on this pool: "
+                        + ("DMMA m16n8k4 f64" if dom["precision"] == "double" else "FMUL+FADD f32") + ")"),
+        "suite_frac": sum(max(r["t_roof_hbm"], r["t_roof_fp"]) for r in rows) / sum(r["seconds"] for r in rows),
+    }
+
+    # e2e through the public API from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        host_x = torch.empty((shard.count, D), dtype=torch.float64, pin_memory=True)
+        host_x.copy_(x64)
+        host_f = torch.empty(args.n, dtype=torch.float64, pin_memory=True)
+        dev_x = x64   # overwritten in place by each step's H2D copy (same values)
+        h2d = shard.count * D * 8
+        d2h = 0
+
+        def e2e_step():
+            nonlocal d2h
+            d2h = 0
+            dev_x.copy_(host_x, non_blocking=True)
+            x32e = dev_x.float()
+            for p in precs:
+                xe = dev_x if p == "double" else x32e
+                for fn in fns:
+                    full = gather_fitness(engine.evaluate(fn, xe, p).values, shard)
+                    dst = host_f[: full.numel()] if p == "double" else host_f.view(torch.float32)[: full.numel()]
+                    dst.copy_(full, non_blocking=True)
+                    d2h += full.numel() * full.element_size()
+            torch.cuda.synchronize()
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": evals / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps}
+        del host_x, host_f
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sample = x64[: args.cpu_rows * (os.cpu_count() or 1)].cpu().numpy()
+        cpu = cpu_reference(D, fns, precs, args.cpu_rows, x_rows=sample)
+
+    if args.breakdown and rank == 0:
+        Path(args.breakdown).write_text(json.dumps({"rows": rows, "n_local": shard.count,
+                                                    "dim": D}, indent=1))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64+f32" if len(precs) == 2 else ("f64" if precs[0] == "double" else "f32"),
+            "data": "synthetic U[-100,100]^D (torch Philox on device, seed 1001+rank)",
+            "config": {"workload": f"suite-sweep D={D} N={args.n} ({len(fns)} fns x {len(precs)} precisions)",
+                       "dim": D, "n": args.n, "fns": len(fns), "precisions": precs,
+                       "parallelism": f"rows/{world}", "l2": "inputs larger than L2 (8 GB fp64 + 4 GB fp32)",
+                       "seed": 0},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+            "per_precision_evals_per_s": {
+                p: len(fns) * args.n / sum(r["seconds"] for r in rows if r["precision"] == p)
+                for p in precs},
+        }
+        print(json.dumps(line), flush=True)
+    engine.dispose()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -12,7 +12,6 @@ Writes
 The reference is imported read-only from /root/reference/pkg/src.
 """
 
-import hashlib
 import json
 import sys
 from pathlib import Path
@@ -20,9 +19,12 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from robench import EngineConfig, initialize  # noqa: E402
 from robench import composition, hybrid, transforms  # noqa: E402
 from robench.transforms import matvec  # noqa: E402
+
+from tests.golden.digest import digest  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 DIMS = (2, 10, 13, 30, 50, 100)
@@ -30,14 +32,6 @@ SEED = 5
 NPTS = 12
 
 
-def digest(arrays) -> str:
-    h = hashlib.sha256()
-    for a in arrays:
-        a = np.ascontiguousarray(a)
-        h.update(str(a.dtype).encode())
-        h.update(str(a.shape).encode())
-        h.update(a.tobytes())
-    return h.hexdigest()
 
 
 def instance_arrays(fn, dim, seed):

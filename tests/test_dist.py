@@ -1,0 +1,67 @@
+"""Row sharding + fitness all-gather (dist.py) on world_size 2 with gloo on
+CPU; the per-rank evaluator is the CPU oracle, so the check is the
+plumbing: partition, rank order, bit-identity with one process."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1407_7737_b200.dist import Shard, ShardedEngine
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+class OracleEngine:
+    def __init__(self, dim):
+        from oracle.robench_oracle import Oracle
+        self.orc = Oracle(dim, 0)
+
+    def evaluate(self, fn, pts, precision=None):
+        class R:
+            pass
+        r = R()
+        r.values = torch.from_numpy(self.orc.evaluate(fn, pts.numpy(), precision or "double"))
+        return r
+
+
+def _worker(rank, world, port, n, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.robench_oracle import population
+    x = population(10, n, seed=3)
+    sh = Shard(rank, world, n)
+    eng = ShardedEngine(OracleEngine(10), sh)
+    local = torch.from_numpy(x[sh.start:sh.start + sh.count])
+    for fn in (0, 23, 30):
+        full = eng.evaluate(fn, local, "double")
+        if rank == 0:
+            np.save(f"{out}_{fn}.npy", full.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [10, 11])
+def test_sharded_evaluation_matches_single_process(tmp_path, n):
+    out = str(tmp_path / "f")
+    mp.spawn(_worker, args=(2, free_port(), n, out), nprocs=2, join=True)
+    from oracle.robench_oracle import Oracle, population
+    x = population(10, n, seed=3)
+    orc = Oracle(10, 0)
+    for fn in (0, 23, 30):
+        assert np.array_equal(np.load(f"{out}_{fn}.npy"), orc.evaluate(fn, x, "double"))
+
+
+def test_shard_partition():
+    for n in (1, 7, 10, 10_000_000):
+        for w in (1, 2, 4, 8):
+            shards = [Shard(r, w, n) for r in range(w)]
+            assert sum(s.count for s in shards) == n
+            assert [s.start for s in shards] == list(np.cumsum([0] + [s.count for s in shards])[:-1])

@@ -10,7 +10,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 from paper_1407_7737_b200 import catalog, instances
-from tests.golden.make_golden import digest
+from tests.golden.digest import digest
 
 GOLDEN = json.loads((ROOT / "tests" / "golden" / "instances.json").read_text())
 

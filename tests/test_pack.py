@@ -1,0 +1,108 @@
+"""Pack invariants and the exact-order rotate schedule: walking a group's
+columns in q-order with the 8-slot fold reproduces NumPy's float32
+``(R * v).sum(axis=1)`` (transforms.py:42-48) bit for bit — the schedule the
+float32 CUDA rotate executes."""
+
+import numpy as np
+import pytest
+
+from paper_1407_7737_b200 import catalog, instances, pack as P
+
+F32 = np.float32
+
+
+def exact_order_rotate(pk, group, v):
+    m = int(group["m"])
+    qb = group["qb"]
+    cols = pk.index[group["col"]:group["col"] + m]
+    rows = pk.index[group["row"]:group["row"] + m]
+    mat = pk.values_f32[group["mat"]:group["mat"] + m * m].reshape(m, m)
+    out = {}
+    for r in range(m):
+        t0 = t1 = t2 = F32(0)
+        for s in range(8):
+            acc = F32(0)
+            for q in range(qb[s], qb[s + 1]):
+                acc = F32(acc + F32(v[cols[q]] * mat[q, r]))
+            if s == 0:
+                t0 = acc
+            elif s == 1:
+                t0 = F32(t0 + acc)
+            elif s in (2, 4):
+                t1 = acc
+            elif s == 3:
+                t1 = F32(t1 + acc)
+                t0 = F32(t0 + t1)
+            elif s == 5:
+                t1 = F32(t1 + acc)
+            elif s == 6:
+                t2 = acc
+            else:
+                t2 = F32(t2 + acc)
+                t1 = F32(t1 + t2)
+                t0 = F32(t0 + t1)
+        for q in range(qb[8], qb[9]):
+            t0 = F32(t0 + F32(v[cols[q]] * mat[q, r]))
+        out[int(rows[r])] = t0
+    return out
+
+
+def dense_for(fn, dim, seed):
+    inst = instances.build(fn, dim, seed)
+    if isinstance(inst, instances.BasicInstance):
+        return inst.rotation.dense()
+    if isinstance(inst, instances.HybridInstance):
+        return inst.chunk_rotations[0]
+    m = inst.members[0]
+    return m.rotation.dense() if m.rotation is not None else m.hybrid.chunk_rotations[0]
+
+
+@pytest.mark.parametrize("dim", [2, 5, 8, 9, 10, 13, 30, 50, 100, 128])
+def test_exact_order_schedule_reproduces_numpy(dim):
+    disabled = frozenset(range(23, 37)) if dim < 10 else frozenset()
+    pk = P.Pack(dim, 1, disabled)
+    rng = np.random.default_rng(dim)
+    for fn in (0, 11, 23, 27, 29, 35):
+        if fn in disabled:
+            continue
+        rec = pk.functions[fn]
+        seg = pk.segments[pk.members[rec["member0"]]["segment0"]]
+        R = dense_for(fn, dim, 1).astype(F32)
+        for _ in range(3):
+            v = rng.uniform(-100, 100, int(seg["d"])).astype(F32)
+            want = (R * v).sum(axis=1)
+            got = np.zeros_like(want)
+            for g in range(seg["n_groups"]):
+                for r, z in exact_order_rotate(pk, pk.groups[seg["group0"] + g], v).items():
+                    got[r] = z
+            assert np.array_equal(got, want)
+
+
+def test_pack_shapes_and_disabled():
+    pk = P.Pack(10, 0)
+    assert len(pk.functions) == 37
+    assert (pk.functions["category"] >= 0).all()
+    pk2 = P.Pack(2, 0, frozenset(range(23, 37)))
+    assert (pk2.functions["category"][23:] == P.DISABLED).all()
+    # block-sparse storage: sum of squared group sizes, never D^2
+    pk100 = P.Pack(100, 0)
+    seg = pk100.segments[pk100.members[pk100.functions[0]["member0"]]["segment0"]]
+    sizes = [int(pk100.groups[seg["group0"] + g]["m"]) for g in range(seg["n_groups"])]
+    assert sizes == [34, 33, 33]
+    assert pk100.max_exact_len == 100
+
+
+def test_kernel_constants_follow_numpy():
+    c = P.kernel_constants("weierstrass", 30, np.float32)
+    k = np.arange(21, dtype=np.float32)
+    assert np.array_equal(c[:21], 0.5**k)
+    assert np.array_equal(c[21:42], 2.0 * np.pi * 3.0**k)
+    assert c.dtype == np.float32
+    e = P.kernel_constants("elliptic", 7, np.float64)
+    assert e[0] == 1.0 and e[-1] == 1e6
+
+
+def test_slot_of():
+    assert [P.slot_of(i, 5) for i in range(5)] == [8] * 5
+    assert [P.slot_of(i, 10) for i in range(10)] == [0, 1, 2, 3, 4, 5, 6, 7, 8, 8]
+    assert P.slot_of(17, 100) == 1 and P.slot_of(96, 100) == 8
