@@ -132,6 +132,10 @@ int32_t rb_abi_version(void);
 void rb_struct_sizes(int64_t out[5]);
 /* Number of kernel launches issued by this process so far (bench evidence). */
 int64_t rb_launch_count(void);
+/* Diagnostic: out[i] = x[i] ** y[i] with NumPy's float32 array-power
+ * semantics (bit-exact SVML powf restatement, csrc/rb_svml_powf.cuh), on
+ * device pointers; synchronous on `stream`. */
+rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

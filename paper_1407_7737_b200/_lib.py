@@ -31,7 +31,7 @@ _STATUS = {
 
 EXPORTS = ("rb_initialize", "rb_dispose", "rb_func_evaluate", "rb_func_evaluatef",
            "rb_h_func_evaluate", "rb_h_func_evaluatef", "rb_last_error",
-           "rb_abi_version", "rb_struct_sizes", "rb_launch_count")
+           "rb_abi_version", "rb_struct_sizes", "rb_launch_count", "rb_np_powf")
 
 
 class RbPack(ctypes.Structure):
@@ -72,6 +72,8 @@ def load() -> ctypes.CDLL:
     lib.rb_abi_version.restype = i32
     lib.rb_struct_sizes.argtypes = [ctypes.POINTER(ctypes.c_int64)]
     lib.rb_launch_count.restype = i64
+    lib.rb_np_powf.argtypes = [vp, vp, vp, i64, vp]
+    lib.rb_np_powf.restype = i32
     _check_layout(lib)
     _lib = lib
     return lib

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(NT, 2) evaluate_kernel(const Args<T> a) {
           w[k] = T(0);
           if (k < nm) {
             const T sg = (T)a.members[fn.member0 + k].sigma;
-            w[k] = M<T>::pow(d2[k], C<T>(-0.5)) * M<T>::exp(-d2[k] / (C<T>(2.0 * D) * (sg * sg)));
+            w[k] = apow<T>(d2[k], C<T>(-0.5)) * M<T>::exp(-d2[k] / (C<T>(2.0 * D) * (sg * sg)));
             tot = tot + w[k];
           }
         }
@@ -362,6 +362,12 @@ __global__ void __launch_bounds__(NT, 2) evaluate_kernel(const Args<T> a) {
     if (l8 == 0 && valid) a.f[row0 + p] = result + C<T>(100.0);     // engine.py:209
     __syncthreads();
   }
+}
+
+__global__ void np_powf_kernel(const float* x, const float* y, float* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = rb_svml::powf_np(x[i], y[i]);
 }
 
 }  // namespace rb
@@ -661,6 +667,18 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
     return s;
   }
   *out = e;
+  return RB_OK;
+}
+
+rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y || !out))) return fail(RB_E_INVALID_ARGUMENT, "bad arguments");
+  if (n == 0) return RB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  rb::np_powf_kernel<<<grid, 256, 0, st>>>(x, y, out, n);
+  g_launches.fetch_add(1);
+  RB_CUDA(cudaGetLastError());
+  RB_CUDA(cudaStreamSynchronize(st));
   return RB_OK;
 }
 

@@ -80,7 +80,7 @@ __device__ T kernel_value(int k, const Pt<T>& P) {
     }
     case K_POWERS: {                                                   // :80-84
       const T* e = P.ctab;
-      return M<T>::sqrt(pw8<T>(0, d, [&](int i) { return M<T>::pow(M<T>::fabs(z[i]), e[i]); }, l8));
+      return M<T>::sqrt(pw8<T>(0, d, [&](int i) { return apow<T>(M<T>::fabs(z[i]), e[i]); }, l8));
     }
     case K_SHARP_VALLEY: {                                             // :87-89
       const T rest = pw8<T>(1, d - 1, [&](int i) { const T a = z[i]; return a * a; }, l8);
@@ -113,7 +113,7 @@ __device__ T kernel_value(int k, const Pt<T>& P) {
       if (d < 2) return T(0);
       const T s = pw8<T>(0, d - 1, [&](int i) {
         const T w = M<T>::sqrt(sq(z[i]) + sq(z[i + 1]));
-        return M<T>::sqrt(w) * (C<T>(1.0) + sq(M<T>::sin(C<T>(50.0) * M<T>::pow(w, C<T>(0.2)))));
+        return M<T>::sqrt(w) * (C<T>(1.0) + sq(M<T>::sin(C<T>(50.0) * apow<T>(w, C<T>(0.2)))));
       }, l8);
       return sq(s / T(d - 1));
     }

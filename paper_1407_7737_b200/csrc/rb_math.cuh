@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "rb_svml_powf.cuh"
+
 #define RB_FULL 0xffffffffu
 
 namespace rb {
@@ -47,6 +49,14 @@ template <> struct M<float> {
   static __device__ __forceinline__ float fmod(float x, float y) { return ::fmodf(x, y); }
   static __device__ __forceinline__ bool finite(float x) { return isfinite(x); }
 };
+
+// Array power ``a ** b`` on NumPy arrays: float64 -> libm-class pow;
+// float32 -> the bit-exact restatement of NumPy's SVML powf
+// (rb_svml_powf.cuh).  Scalar powers (np.float32 ** float) go through libm
+// powf in NumPy and use M<T>::pow here.
+template <class T> __device__ __forceinline__ T apow(T a, T b);
+template <> __device__ __forceinline__ double apow<double>(double a, double b) { return ::pow(a, b); }
+template <> __device__ __forceinline__ float apow<float>(float a, float b) { return rb_svml::powf_np(a, b); }
 
 // Python-double constant as NumPy casts it into the working dtype (NEP 50:
 // the weak Python float is rounded once to T).
