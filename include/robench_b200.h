@@ -58,7 +58,12 @@ typedef struct rb_group {
   int32_t qb[10];   /* slot s spans q in [qb[s], qb[s+1]) for s < 8; tail [qb[8], qb[9]); qb[9] == m */
   int32_t col;      /* index[col + q]: input position (into the segment vector v) of the q-th column */
   int32_t row;      /* index[row + r]: output position (into z) of block row r */
-  int32_t mat;      /* values[mat + q*m + r] = block[r][column of q] */
+  int32_t mat;      /* values[mat + q*m4 + r] = block[r][column of q], m4 = m rounded up to 4
+                       (rows zero-padded; float32 exact-order rotate, 16-byte aligned) */
+  int32_t frag;     /* values[frag + ((nt*nks + ks)*32 + lane)] = mat[4ks + lane%4][8nt + lane/4]
+                       (zero outside m x m): the mma.m16n8k4 B fragments, nt < ceil(m/8),
+                       ks < ceil(m/4) (float64 DMMA rotate) */
+  int32_t reserved;
 } rb_group;
 
 /* One kernel application: v = scale*((x - o)[src..]) + pre; z = R v + post;

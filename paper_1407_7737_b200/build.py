@@ -16,12 +16,12 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
 LIB = HERE / "librobench_b200.so"
-SOURCES = [HERE / "csrc" / "rb_eval.cu"]
+SOURCES = [HERE / "csrc" / n for n in ("rb_capi.cu", "rb_kern_f64.cu", "rb_kern_f32.cu")]
 DEPS = SOURCES + sorted((HERE / "csrc").glob("*.cuh")) + [ROOT / "include" / "robench_b200.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-    "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-v",
     "-I", str(ROOT / "include"),
 ]
 
@@ -38,15 +38,31 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
+def _compile(src: Path) -> tuple[Path, str]:
+    obj = HERE / "build" / (src.stem + ".o")
+    obj.parent.mkdir(exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", str(obj), str(src)]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"nvcc failed on {src.name} ({proc.returncode}):\n{proc.stderr[-4000:]}")
+    return obj, proc.stdout + proc.stderr
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile the translation units in parallel, then link the shared library."""
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB), *map(str, SOURCES), "-lcudart"]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
-    log = proc.stdout + proc.stderr
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        results = list(pool.map(_compile, SOURCES))
+    log = "".join(f"== {src.name}\n{out}" for src, (_, out) in zip(SOURCES, results))
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB),
+            *[str(o) for o, _ in results], "-lcudart"]
+    proc = subprocess.run(link, capture_output=True, text=True)
+    log += proc.stdout + proc.stderr
     (HERE / "build.log").write_text(log)
     if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{log[-4000:]}")
+        raise RuntimeError(f"link failed ({proc.returncode}):\n{log[-4000:]}")
     if verbose:
         print(log)
     return LIB

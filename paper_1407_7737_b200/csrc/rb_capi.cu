@@ -1,0 +1,381 @@
+// Host side of the C ABI (include/robench_b200.h): engine lifecycle, pack
+// upload, validation in the reference's order, kernel selection and launch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rb_device.cuh"
+
+namespace rb {
+extern const void* const kernels_f64[N_VARIANTS];
+extern const void* const kernels_f32[N_VARIANTS];
+
+__global__ void np_powf_kernel(const float* x, const float* y, float* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = rb_svml::powf_np(x[i], y[i]);
+}
+}  // namespace rb
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+constexpr int kFlagSlots = 4096;
+
+rb_status fail(rb_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define RB_CUDA(call)                                                               \
+  do {                                                                              \
+    cudaError_t err_ = (call);                                                      \
+    if (err_ != cudaSuccess)                                                        \
+      return fail(RB_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(err_)); \
+  } while (0)
+
+template <class X>
+rb_status upload(X** dst, const X* src, int64_t count) {
+  *dst = nullptr;
+  if (count <= 0) return RB_OK;
+  RB_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), sizeof(X) * count));
+  RB_CUDA(cudaMemcpy(*dst, src, sizeof(X) * count, cudaMemcpyHostToDevice));
+  return RB_OK;
+}
+
+int pad_to(int v, int mod, int rem) {   // smallest u >= v with u % mod == rem
+  int u = v;
+  while (u % mod != rem) ++u;
+  return u;
+}
+
+// Launch configuration of one (function, precision).
+struct Launch {
+  const void* func = nullptr;
+  size_t smem = 0;
+  int grid_cap = 0;
+  int ldv = 0, max_q = 0;
+};
+
+}  // namespace
+
+struct rb_engine {
+  int device = 0;
+  int dim = 0;
+  int64_t max_concurrency = 0;
+  int ldz[2] = {0, 0};                       // [0] fp64, [1] fp32
+  std::vector<rb_function> fns;              // host copy for validation
+  std::vector<int> exact_ok;                 // fp32 exact-order rotate supported
+  std::vector<Launch> launch[2];
+  rb_function* d_fns = nullptr;
+  rb_member* d_members = nullptr;
+  rb_segment* d_segments = nullptr;
+  rb_group* d_groups = nullptr;
+  int32_t* d_index = nullptr;
+  double* d_v64 = nullptr;
+  float* d_v32 = nullptr;
+  int* d_flags = nullptr;                    // ring of per-call non-finite flags
+  int* h_flags = nullptr;                    // pinned mirror
+  std::atomic<int> next_flag{0};
+  std::mutex host_mu;                        // host-pointer API staging buffers
+  void* stage_x = nullptr;
+  void* stage_f = nullptr;
+  size_t stage_bytes_x = 0, stage_bytes_f = 0;
+  cudaStream_t host_stream = nullptr;
+};
+
+namespace {
+
+void release(rb_engine* e) {
+  if (!e) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(e->device);
+  cudaFree(e->d_fns);
+  cudaFree(e->d_members);
+  cudaFree(e->d_segments);
+  cudaFree(e->d_groups);
+  cudaFree(e->d_index);
+  cudaFree(e->d_v64);
+  cudaFree(e->d_v32);
+  cudaFree(e->d_flags);
+  cudaFree(e->stage_x);
+  cudaFree(e->stage_f);
+  if (e->h_flags) cudaFreeHost(e->h_flags);
+  if (e->host_stream) cudaStreamDestroy(e->host_stream);
+  cudaSetDevice(prev);
+  delete e;
+}
+
+template <class T>
+rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
+                          cudaStream_t stream) {
+  // validation in the reference's order (engine.py:180-203)
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (fn_id < 0 || fn_id >= (int32_t)e->fns.size())
+    return fail(RB_E_UNKNOWN_FUNCTION, "function id " + std::to_string(fn_id) + " is not in 0..36");
+  if (e->fns[fn_id].category == RB_DISABLED)
+    return fail(RB_E_DISABLED_FUNCTION, "function " + std::to_string(fn_id) + " needs dimension >= 10");
+  if (n > e->max_concurrency)
+    return fail(RB_E_BATCH_TOO_LARGE, "batch of " + std::to_string(n) + " exceeds max_concurrency=" +
+                                          std::to_string(e->max_concurrency));
+  if (n < 1 || !x || !f) return fail(RB_E_INVALID_ARGUMENT, "empty batch or null pointer");
+  const int pi = sizeof(T) == 8 ? 0 : 1;
+  if (pi == 1 && !e->exact_ok[fn_id])
+    return fail(RB_E_UNSUPPORTED, "single precision needs rotation blocks of length <= 128");
+  const Launch& L = e->launch[pi][fn_id];
+
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
+  const int slot = e->next_flag.fetch_add(1) % kFlagSlots;
+  int* dflag = e->d_flags + slot;
+  RB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), stream));
+
+  rb::Args<T> a;
+  a.x = x;
+  a.f = f;
+  a.n = n;
+  a.dim = e->dim;
+  a.fns = e->d_fns;
+  a.members = e->d_members;
+  a.segments = e->d_segments;
+  a.groups = e->d_groups;
+  a.index = e->d_index;
+  a.values = reinterpret_cast<const T*>(pi == 0 ? (const void*)e->d_v64 : (const void*)e->d_v32);
+  a.fn = fn_id;
+  a.flag = dflag;
+  a.ldz = e->ldz[pi];
+  a.ldv = L.ldv;
+  a.max_q = L.max_q;
+  a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+  const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
+  const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
+  void* args[] = {&a};
+  RB_CUDA(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream));
+  g_launches.fetch_add(1);
+  RB_CUDA(cudaMemcpyAsync(e->h_flags + slot, dflag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  RB_CUDA(cudaStreamSynchronize(stream));
+  const int flag = e->h_flags[slot];
+  if (prev != e->device) cudaSetDevice(prev);
+  if (flag & 1) return fail(RB_E_NON_FINITE_INPUT, "batch contains NaN or infinity");
+  if (flag & 2) return fail(RB_E_NON_FINITE_INPUT, "kernel input contains NaN or infinity");
+  return RB_OK;
+}
+
+template <class T>
+rb_status evaluate_host(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (n < 1 || n > e->max_concurrency || !x || !f || fn_id < 0 ||
+      fn_id >= (int32_t)e->fns.size() || e->fns[fn_id].category == RB_DISABLED)
+    return evaluate_device<T>(e, fn_id, x, n, f, nullptr);   // reports the error
+  std::lock_guard<std::mutex> lock(e->host_mu);
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  RB_CUDA(cudaSetDevice(e->device));
+  const size_t bx = sizeof(T) * (size_t)n * e->dim, bf = sizeof(T) * (size_t)n;
+  if (bx > e->stage_bytes_x) {
+    cudaFree(e->stage_x);
+    e->stage_x = nullptr;
+    RB_CUDA(cudaMalloc(&e->stage_x, bx));
+    e->stage_bytes_x = bx;
+  }
+  if (bf > e->stage_bytes_f) {
+    cudaFree(e->stage_f);
+    e->stage_f = nullptr;
+    RB_CUDA(cudaMalloc(&e->stage_f, bf));
+    e->stage_bytes_f = bf;
+  }
+  RB_CUDA(cudaMemcpyAsync(e->stage_x, x, bx, cudaMemcpyHostToDevice, e->host_stream));
+  const rb_status s = evaluate_device<T>(e, fn_id, static_cast<const T*>(e->stage_x), n,
+                                         static_cast<T*>(e->stage_f), e->host_stream);
+  if (s == RB_OK) RB_CUDA(cudaMemcpyAsync(f, e->stage_f, bf, cudaMemcpyDeviceToHost, e->host_stream));
+  RB_CUDA(cudaStreamSynchronize(e->host_stream));
+  cudaSetDevice(prev);
+  return s;
+}
+
+// Per-function launch parameters: kernel variant, shared-memory layout.
+rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
+  int sms = 0, optin = 0;
+  RB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  RB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  int max_d = 1;
+  for (int i = 0; i < pk->n_segments; ++i) max_d = std::max(max_d, pk->segments[i].d);
+  e->ldz[0] = pad_to(max_d, 16, 8);   // 8 lanes x 4 points read rows: stride 8 (mod 16) doubles
+  e->ldz[1] = pad_to(max_d, 32, 8);
+  const int nf = pk->n_functions;
+  e->exact_ok.assign(nf, 1);
+  for (int pi = 0; pi < 2; ++pi) e->launch[pi].assign(nf, Launch());
+  std::vector<size_t> need[2] = {std::vector<size_t>(rb::N_VARIANTS, 0),
+                                 std::vector<size_t>(rb::N_VARIANTS, 0)};
+  std::vector<int> variant(nf, rb::N_VARIANTS - 1);
+  for (int fi = 0; fi < nf; ++fi) {
+    const rb_function& fn = pk->functions[fi];
+    if (fn.category == RB_DISABLED) continue;
+    const rb_member& first = pk->members[fn.member0];
+    const rb_member& last = pk->members[fn.member0 + fn.n_members - 1];
+    const int s0 = first.segment0, s1 = last.segment0 + last.n_segments;
+    const int g0 = pk->segments[s0].group0;
+    const int g1 = pk->segments[s1 - 1].group0 + pk->segments[s1 - 1].n_groups;
+    if (fn.n_members > rb::MAX_MEMBERS || s1 - s0 > rb::MAX_SEGMENTS || g1 - g0 > rb::MAX_GROUPS)
+      return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the plan limits");
+    int max_q = 0, ldv = 4;
+    for (int si = s0; si < s1; ++si) {
+      const rb_segment& sg = pk->segments[si];
+      int q4 = 0;
+      for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
+        max_q += pk->groups[g].m;
+        q4 += (pk->groups[g].m + 3) & ~3;
+      }
+      ldv = std::max(ldv, q4);
+      if (sg.n_groups && sg.d > 128) e->exact_ok[fi] = 0;
+    }
+    if (fn.category == RB_BASIC && fn.n_members == 1 && first.n_segments == 1)
+      variant[fi] = pk->segments[s0].kernel;
+    for (int pi = 0; pi < 2; ++pi) {
+      Launch& L = e->launch[pi][fi];
+      L.func = (pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[variant[fi]];
+      L.max_q = std::max(max_q, 1);
+      L.ldv = ldv;
+      L.smem = pi == 0 ? rb::smem_bytes<double>(pk->dim, ldv, e->ldz[0], L.max_q)
+                       : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q);
+      if ((int)L.smem > optin)
+        return fail(RB_E_UNSUPPORTED, "dimension too large for the shared-memory tile");
+      need[pi][variant[fi]] = std::max(need[pi][variant[fi]], L.smem);
+    }
+  }
+  for (int pi = 0; pi < 2; ++pi)
+    for (int v = 0; v < rb::N_VARIANTS; ++v)
+      if (need[pi][v])
+        RB_CUDA(cudaFuncSetAttribute((pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[v],
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need[pi][v]));
+  for (int fi = 0; fi < nf; ++fi) {
+    if (pk->functions[fi].category == RB_DISABLED) continue;
+    for (int pi = 0; pi < 2; ++pi) {
+      Launch& L = e->launch[pi][fi];
+      int per_sm = 0;
+      RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.func, rb::NT, L.smem));
+      if (per_sm < 1) return fail(RB_E_UNSUPPORTED, "kernel does not fit on an SM");
+      L.grid_cap = sms * per_sm;
+    }
+  }
+  return RB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t rb_abi_version(void) { return 1; }
+
+const char* rb_last_error(void) { return g_last_error.c_str(); }
+
+int64_t rb_launch_count(void) { return g_launches.load(); }
+
+void rb_struct_sizes(int64_t out[5]) {
+  out[0] = sizeof(rb_group);
+  out[1] = sizeof(rb_segment);
+  out[2] = sizeof(rb_member);
+  out[3] = sizeof(rb_function);
+  out[4] = sizeof(rb_pack);
+}
+
+rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t device,
+                        rb_engine** out) {
+  if (!pk || !out) return fail(RB_E_INVALID_ARGUMENT, "null pack or output pointer");
+  *out = nullptr;
+  if (pk->dim < 2 || pk->n_functions <= 0 || max_concurrency < 1)
+    return fail(RB_E_INVALID_ARGUMENT, "malformed pack");
+  for (int i = 0; i < pk->n_functions; ++i) {
+    const rb_function& f = pk->functions[i];
+    if (f.category == RB_DISABLED) continue;
+    if (f.n_members < 1 || f.member0 < 0 || f.member0 + f.n_members > pk->n_members)
+      return fail(RB_E_INVALID_ARGUMENT, "function " + std::to_string(i) + ": bad members");
+  }
+  for (int i = 0; i < pk->n_segments; ++i) {
+    const rb_segment& s = pk->segments[i];
+    if (s.kernel < 0 || s.kernel >= rb::K_COUNT || s.d < 1 || s.d > pk->dim ||
+        s.group0 + s.n_groups > pk->n_groups)
+      return fail(RB_E_INVALID_ARGUMENT, "segment " + std::to_string(i) + " malformed");
+  }
+  int ndev = 0;
+  RB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return fail(RB_E_INVALID_ARGUMENT, "device " + std::to_string(device) + " not present");
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  RB_CUDA(cudaSetDevice(device));
+
+  rb_engine* e = new rb_engine();
+  e->device = device;
+  e->dim = pk->dim;
+  e->max_concurrency = max_concurrency;
+  e->fns.assign(pk->functions, pk->functions + pk->n_functions);
+  rb_status s = plan_launches(e, pk, device);
+  if (s == RB_OK) s = upload(&e->d_fns, pk->functions, pk->n_functions);
+  if (s == RB_OK) s = upload(&e->d_members, pk->members, pk->n_members);
+  if (s == RB_OK) s = upload(&e->d_segments, pk->segments, pk->n_segments);
+  if (s == RB_OK) s = upload(&e->d_groups, pk->groups, pk->n_groups);
+  if (s == RB_OK) s = upload(&e->d_index, pk->index, pk->n_index);
+  if (s == RB_OK) s = upload(&e->d_v64, pk->values_f64, pk->n_values);
+  if (s == RB_OK) s = upload(&e->d_v32, pk->values_f32, pk->n_values);
+  if (s == RB_OK && cudaMalloc(&e->d_flags, sizeof(int) * kFlagSlots) != cudaSuccess)
+    s = fail(RB_E_CUDA, "flag allocation failed");
+  if (s == RB_OK && cudaMallocHost(&e->h_flags, sizeof(int) * kFlagSlots) != cudaSuccess)
+    s = fail(RB_E_CUDA, "pinned flag allocation failed");
+  if (s == RB_OK && cudaStreamCreateWithFlags(&e->host_stream, cudaStreamNonBlocking) != cudaSuccess)
+    s = fail(RB_E_CUDA, "stream creation failed");
+  cudaSetDevice(prev);
+  if (s != RB_OK) {
+    release(e);
+    return s;
+  }
+  *out = e;
+  return RB_OK;
+}
+
+rb_status rb_dispose(rb_engine** engine) {
+  if (!engine || !*engine) return RB_OK;
+  release(*engine);
+  *engine = nullptr;
+  return RB_OK;
+}
+
+rb_status rb_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64_t n, double* f,
+                           void* stream) {
+  return evaluate_device<double>(e, fn_id, x, n, f, static_cast<cudaStream_t>(stream));
+}
+
+rb_status rb_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f,
+                            void* stream) {
+  return evaluate_device<float>(e, fn_id, x, n, f, static_cast<cudaStream_t>(stream));
+}
+
+rb_status rb_h_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64_t n, double* f) {
+  return evaluate_host<double>(e, fn_id, x, n, f);
+}
+
+rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f) {
+  return evaluate_host<float>(e, fn_id, x, n, f);
+}
+
+rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y || !out))) return fail(RB_E_INVALID_ARGUMENT, "bad arguments");
+  if (n == 0) return RB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  rb::np_powf_kernel<<<grid, 256, 0, st>>>(x, y, out, n);
+  g_launches.fetch_add(1);
+  RB_CUDA(cudaGetLastError());
+  RB_CUDA(cudaStreamSynchronize(st));
+  return RB_OK;
+}
+
+}  // extern "C"

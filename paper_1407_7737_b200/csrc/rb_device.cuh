@@ -1,0 +1,522 @@
+// The evaluation kernel (device side), shared by the per-precision
+// instantiation units rb_kern_f64.cu / rb_kern_f32.cu.
+//
+// Persistent grid; one CTA (256 threads) walks tiles of TP = 32 points:
+//   load     X tile -> XS via one TMA bulk copy (cp.async.bulk + mbarrier)
+//   rotate   z = R (scale*(x - o)[perm] + pre) + post per diagonal block
+//              fp64: warp strips of 16 points x 40 rows on the tensor pipe,
+//                    mma.sync.m16n8k4.f64 (DMMA); the shift/scale is applied
+//                    while building the A fragments straight from XS, the B
+//                    fragments come pre-swizzled from the pack (one 256-byte
+//                    coalesced load per fragment)
+//              fp32: SIMT FMUL+FADD in NumPy's pairwise order (bit-exact z),
+//                    4 points x 4 rows per thread from a q-ordered V tile
+//   kernel   8 lanes per point, NumPy-order reductions (rb_kernels.cuh)
+//   blend    composition weights / member sum (composition.py:114-166)
+// The function's descriptors and per-column gather tables are copied into
+// shared memory once per CTA ("plan").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/robench_b200.h"
+#include "rb_kernels.cuh"
+
+namespace rb {
+
+constexpr int TP = 32;          // points per tile
+constexpr int NT = 256;         // threads per CTA = 8 lanes x TP
+constexpr int MAX_MEMBERS = 5;
+constexpr int MAX_SEGMENTS = 16;
+constexpr int MAX_GROUPS = 16;
+constexpr int NTC = 5;          // DMMA n-tiles (8 rows) per warp strip
+constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
+
+template <class T>
+struct Args {
+  const T* x;
+  T* f;
+  int64_t n;
+  int dim;
+  const rb_function* fns;
+  const rb_member* members;
+  const rb_segment* segments;
+  const rb_group* groups;
+  const int32_t* index;
+  const T* values;
+  int fn;
+  int* flag;        // bit 0: non-finite x, bit 1: non-finite kernel input
+  int ldz;          // ZS row stride (elements)
+  int ldv;          // fp32 V tile rows (sum of 4-padded group sizes)
+  int max_q;        // capacity of the plan's gather tables
+  int tma;          // x is 16-byte aligned: bulk-copy full tiles
+};
+
+struct PlanHead {
+  rb_function fn;
+  int seg_base, grp_base, n_seg, n_grp;
+  rb_member mem[MAX_MEMBERS];
+  rb_segment seg[MAX_SEGMENTS];
+  rb_group grp[MAX_GROUPS];
+  int gq0[MAX_GROUPS];            // group g's slice of the gather tables
+  unsigned long long mbar;        // TMA completion barrier
+};
+
+// dynamic shared memory: [PlanHead][qsrc int[max_q]][qo T[max_q]][XS][V][ZS]
+template <class T>
+struct Smem {
+  PlanHead* P;
+  int* qsrc;      // x column feeding the group's q-th column (split perm applied)
+  T* qo;          // the optimum at that column
+  T* XS;          // [TP][dim]
+  T* VS;          // fp32 only: [ldv][TP]
+  T* ZS;          // [TP][ldz]
+};
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+template <class T>
+__host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q) {
+  size_t b = align16(sizeof(PlanHead));
+  b += align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
+  b += align16(sizeof(T) * TP * dim);
+  if (sizeof(T) == 4) b += align16(sizeof(T) * TP * ldv);
+  b += align16(sizeof(T) * TP * ldz);
+  return b;
+}
+
+template <class T>
+__device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
+  Smem<T> s;
+  size_t off = 0;
+  s.P = reinterpret_cast<PlanHead*>(base);
+  off += align16(sizeof(PlanHead));
+  s.qsrc = reinterpret_cast<int*>(base + off);
+  off += align16(sizeof(int) * a.max_q);
+  s.qo = reinterpret_cast<T*>(base + off);
+  off += align16(sizeof(T) * a.max_q);
+  s.XS = reinterpret_cast<T*>(base + off);
+  off += align16(sizeof(T) * TP * a.dim);
+  s.VS = reinterpret_cast<T*>(base + off);
+  if (sizeof(T) == 4) off += align16(sizeof(T) * TP * a.ldv);
+  s.ZS = reinterpret_cast<T*>(base + off);
+  return s;
+}
+
+__device__ __forceinline__ int round4(int v) { return (v + 3) & ~3; }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ------------------------------------------------------------------ plan
+// Copy the function's descriptors (contiguous in the pack) into shared
+// memory and build the per-group gather tables.
+template <class T>
+__device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
+  PlanHead& P = *s.P;
+  if (threadIdx.x == 0) {
+    const rb_function fn = a.fns[a.fn];
+    P.fn = fn;
+    const rb_member first = a.members[fn.member0];
+    const rb_member last = a.members[fn.member0 + fn.n_members - 1];
+    P.seg_base = first.segment0;
+    P.n_seg = last.segment0 + last.n_segments - first.segment0;
+    const rb_segment s0 = a.segments[first.segment0];
+    const rb_segment sl = a.segments[last.segment0 + last.n_segments - 1];
+    P.grp_base = s0.group0;
+    P.n_grp = sl.group0 + sl.n_groups - s0.group0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.fn.n_members; i += NT) P.mem[i] = a.members[P.fn.member0 + i];
+  for (int i = threadIdx.x; i < P.n_seg; i += NT) P.seg[i] = a.segments[P.seg_base + i];
+  for (int i = threadIdx.x; i < P.n_grp; i += NT) P.grp[i] = a.groups[P.grp_base + i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int q = 0;
+    for (int g = 0; g < P.n_grp; ++g) {
+      P.gq0[g] = q;
+      q += P.grp[g].m;
+    }
+  }
+  __syncthreads();
+  // gather tables: walk members -> segments -> groups
+  for (int mi = 0; mi < P.fn.n_members; ++mi) {
+    const rb_member& mem = P.mem[mi];
+    const T* o = a.values + mem.shift;
+    for (int si = 0; si < mem.n_segments; ++si) {
+      const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
+      for (int gi = 0; gi < seg.n_groups; ++gi) {
+        const int g = seg.group0 - P.grp_base + gi;
+        const rb_group& G = P.grp[g];
+        const int32_t* cols = a.index + G.col;
+        for (int q = threadIdx.x; q < G.m; q += NT) {
+          const int pos = cols[q];
+          const int src = mem.perm >= 0 ? a.index[mem.perm + seg.src + pos] : pos;
+          s.qsrc[P.gq0[g] + q] = src;
+          s.qo[P.gq0[g] + q] = o[src];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- X tile load
+template <class T>
+__device__ void load_tile(const Args<T>& a, const Smem<T>& s, int64_t row0, int nv,
+                          uint32_t& phase) {
+  const int D = a.dim;
+  const uint32_t bytes = (uint32_t)(sizeof(T) * (size_t)nv * D);
+  const T* src = a.x + row0 * D;
+  if (a.tma && (bytes & 15u) == 0) {
+    if (threadIdx.x == 0) {
+      const uint32_t bar = smem_u32(&s.P->mbar);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(s.XS)),
+          "l"(src), "r"(bytes), "r"(bar)
+          : "memory");
+    }
+    const uint32_t bar = smem_u32(&s.P->mbar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar), "r"(phase)
+          : "memory");
+    }
+    phase ^= 1u;
+  } else {
+    for (int e = threadIdx.x; e < nv * D; e += NT) s.XS[e] = src[e];
+    __syncthreads();
+  }
+  // finiteness of the batch (engine.py:202-203)
+  bool bad = false;
+  for (int e = threadIdx.x; e < nv * D; e += NT) bad |= !M<T>::finite(s.XS[e]);
+  if (bad) atomicOr(a.flag, 1);
+}
+
+// ------------------------------------------------------------ rotate fp64
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+// z[p][row] = post + sum_q (scale*(x[p][src_q] - o_q) + pre) * B[q][r]
+// Warp task = (group, 16-point m-tile, chunk of NTC n-tiles).  A fragments
+// (a_i = (point gid + 8i, column tig)) are formed in registers from XS; B
+// fragments are pre-swizzled in the pack (rb_group::frag).
+__device__ inline void rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
+  const PlanHead& P = *s.P;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const double scale = seg.scale, pre = seg.pre, post = seg.post;
+  const int g0 = seg.group0 - P.grp_base;
+  int total = 0;
+  for (int g = 0; g < seg.n_groups; ++g) {
+    const int ntn = (P.grp[g0 + g].m + 7) >> 3;
+    total += (TP / 16) * ((ntn + NTC - 1) / NTC);
+  }
+  for (int t = warp; t < total; t += NT / 32) {
+    int g = g0, rem = t;
+    for (;;) {
+      const int ntn = (P.grp[g].m + 7) >> 3;
+      const int cnt = (TP / 16) * ((ntn + NTC - 1) / NTC);
+      if (rem < cnt) break;
+      rem -= cnt;
+      ++g;
+    }
+    const rb_group& G = P.grp[g];
+    const int m = G.m, ntn = (m + 7) >> 3, nks = (m + 3) >> 2;
+    const int nch = (ntn + NTC - 1) / NTC;
+    const int mt = rem / nch, ch = rem - mt * nch;
+    const int nt0 = ch * NTC, ncnt = min(NTC, ntn - nt0);
+    const double* F = a.values + G.frag + (size_t)nt0 * nks * 32 + lane;
+    const int* qs = s.qsrc + P.gq0[g];
+    const double* qo = s.qo + P.gq0[g];
+    const double* X0 = s.XS + (mt * 16 + gid) * a.dim;
+    const double* X1 = X0 + 8 * a.dim;
+    double acc[NTC][4];
+#pragma unroll
+    for (int c = 0; c < NTC; ++c)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[c][i] = 0.0;
+    for (int ks = 0; ks < nks; ++ks) {
+      const int q = ks * 4 + tig;
+      double a0 = 0.0, a1 = 0.0;
+      if (q < m) {
+        const int col = qs[q];
+        const double o = qo[q];
+        a0 = scale * (X0[col] - o);
+        a1 = scale * (X1[col] - o);
+        if (pre != 0.0) {
+          a0 = a0 + pre;
+          a1 = a1 + pre;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NTC; ++c)
+        if (c < ncnt) dmma_16x8x4(acc[c], a0, a1, __ldg(F + (c * nks + ks) * 32));
+    }
+    const int32_t* rows = a.index + G.row;
+#pragma unroll
+    for (int c = 0; c < NTC; ++c) {
+      if (c >= ncnt) break;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rr = (nt0 + c) * 8 + 2 * tig + (i & 1);
+        const int pp = mt * 16 + gid + ((i >> 1) << 3);
+        if (rr < m) s.ZS[pp * a.ldz + __ldg(rows + rr)] = post != 0.0 ? acc[c][i] + post : acc[c][i];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ rotate fp32
+// Exact NumPy order (transforms.py:42-48): rounded products, per-slot
+// accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
+// ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
+__device__ inline void rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
+  const PlanHead& P = *s.P;
+  const int g0 = seg.group0 - P.grp_base;
+  const float scale = (float)seg.scale, pre = (float)seg.pre, post = (float)seg.post;
+  // gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre
+  {
+    int vq = 0;
+    for (int g = 0; g < seg.n_groups; ++g) {
+      const rb_group& G = P.grp[g0 + g];
+      const int kp = round4(G.m);
+      const int* qs = s.qsrc + P.gq0[g0 + g];
+      const float* qo = s.qo + P.gq0[g0 + g];
+      for (int e = threadIdx.x; e < TP * kp; e += NT) {
+        const int q = e / TP, p = e - q * TP;
+        float v = 0.0f;
+        if (q < G.m) {
+          v = scale * (s.XS[p * a.dim + qs[q]] - qo[q]);
+          if (pre != 0.0f) v = v + pre;
+        }
+        s.VS[(vq + q) * TP + p] = v;
+      }
+      vq += kp;
+    }
+  }
+  __syncthreads();
+  int total = 0;
+  for (int g = 0; g < seg.n_groups; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
+  for (int t = threadIdx.x; t < total; t += NT) {
+    int g = g0, rem = t, vq = 0;
+    for (;;) {
+      const int cnt = (TP / 4) * ((P.grp[g].m + 3) >> 2);
+      if (rem < cnt) break;
+      rem -= cnt;
+      vq += round4(P.grp[g].m);
+      ++g;
+    }
+    const rb_group& G = P.grp[g];
+    const int pq = rem & 7, rq = rem >> 3;
+    const int m = G.m, m4 = round4(m);
+    const float* B = a.values + G.mat + rq * 4;
+    float t0[4][4], t1[4][4], t2[4][4], acc[4][4];
+#pragma unroll
+    for (int sl = 0; sl < 8; ++sl) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+      for (int q = G.qb[sl]; q < G.qb[sl + 1]; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(B + q * m4));
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(vv[i], bb[j]));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float x = acc[i][j];
+          switch (sl) {
+            case 0: t0[i][j] = x; break;
+            case 1: t0[i][j] = __fadd_rn(t0[i][j], x); break;
+            case 2: t1[i][j] = x; break;
+            case 3: t1[i][j] = __fadd_rn(t1[i][j], x); t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]); break;
+            case 4: t1[i][j] = x; break;
+            case 5: t1[i][j] = __fadd_rn(t1[i][j], x); break;
+            case 6: t2[i][j] = x; break;
+            default:
+              t2[i][j] = __fadd_rn(t2[i][j], x);
+              t1[i][j] = __fadd_rn(t1[i][j], t2[i][j]);
+              t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]);
+          }
+        }
+    }
+    for (int q = G.qb[8]; q < G.qb[9]; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(B + q * m4));
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], bb[j]));
+    }
+    const int32_t* rows = a.index + G.row;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (rq * 4 + j >= m) break;
+      const int row = __ldg(rows + rq * 4 + j);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        s.ZS[(pq * 4 + i) * a.ldz + row] = post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------- one segment
+template <class T>
+__device__ void stage_segment(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
+                              const rb_segment& seg) {
+  if (seg.n_groups == 0) {                 // shift-only ids 10 and 15
+    const T* o = a.values + mem.shift;
+    const int32_t* perm = mem.perm >= 0 ? a.index + mem.perm + seg.src : nullptr;
+    const T scale = (T)seg.scale, pre = (T)seg.pre, post = (T)seg.post;
+    const int d = seg.d;
+    for (int e = threadIdx.x; e < TP * d; e += NT) {
+      const int p = e / d, j = e - p * d;
+      const int src = perm ? perm[j] : j;
+      T v = scale * (s.XS[p * a.dim + src] - o[src]);
+      if (pre != T(0)) v = v + pre;
+      if (post != T(0)) v = v + post;
+      s.ZS[p * a.ldz + j] = v;
+    }
+  } else {
+    rotate(a, s, seg);
+  }
+  __syncthreads();
+}
+
+template <class T, int KID>
+__device__ __forceinline__ T segment_value(const Smem<T>& s, const rb_segment& seg, const T* ctab,
+                                           int p, int l8, const Args<T>& a, bool live) {
+  const T* z = s.ZS + p * a.ldz;
+  bool bad = false;
+  for (int j = l8; j < seg.d; j += 8) bad |= !M<T>::finite(z[j]);   // kernels.py:45-49
+  if (bad && live) atomicOr(a.flag, 2);
+  const Pt<T> pt{z, seg.d, l8, ctab};
+  if constexpr (KID >= 0) return kernel_value_k<T, KID>(pt);
+  else return kernel_value<T>(seg.kernel, pt);
+}
+
+// Value of one member (basic function, hybrid, or composition member).
+template <class T, int KID>
+__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, bool live) {
+  const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const PlanHead& P = *s.P;
+  T total = T(0);
+  for (int si = 0; si < mem.n_segments; ++si) {
+    const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
+    stage_segment(a, s, mem, seg);
+    const T v = segment_value<T, KID>(s, seg, a.values + seg.ctab, p, l8, a, live);
+    total = (si == 0) ? v : total + v;   // hybrid.py:105-115: 0 + K_0 + K_1 + ...
+    __syncthreads();                      // ZS is rewritten by the next segment
+  }
+  return total;
+}
+
+template <class T, int KID>
+__global__ void __launch_bounds__(NT, 2) evaluate_kernel(const Args<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Smem<T> s = carve<T>(smem_raw, a);
+  load_plan(a, s);
+  const PlanHead& P = *s.P;
+  const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const int64_t ntiles = (a.n + TP - 1) / TP;
+  uint32_t phase = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * TP;
+    const int64_t left = a.n - row0;
+    const int nv = left < TP ? (int)left : TP;
+    load_tile(a, s, row0, nv, phase);
+    __syncthreads();
+    const bool valid = p < nv;
+    T result;
+    if constexpr (KID >= 0) {
+      result = member_value<T, KID>(a, s, P.mem[0], valid);
+    } else if (P.fn.category != RB_COMPOSITION) {
+      result = member_value<T, GENERIC>(a, s, P.mem[0], valid);
+    } else {
+      // composition.py:114-141: weights from the squared distances
+      const int nm = P.fn.n_members;
+      const T* x = s.XS + p * a.dim;
+      T d2[MAX_MEMBERS], om[MAX_MEMBERS];
+#pragma unroll
+      for (int k = 0; k < MAX_MEMBERS; ++k) {
+        d2[k] = T(0);
+        om[k] = T(0);
+        if (k < nm) {
+          const T* o = a.values + P.mem[k].shift;
+          d2[k] = pw8<T>(0, a.dim, [&](int j) { const T t = x[j] - o[j]; return t * t; }, l8);
+        }
+      }
+      T mn = d2[0];
+      int am = 0;
+#pragma unroll
+      for (int k = 1; k < MAX_MEMBERS; ++k)
+        if (k < nm && d2[k] < mn) { mn = d2[k]; am = k; }
+      if (mn < C<T>(1.0000000000000002e-24)) {          // 1e-12**2: on an optimum
+#pragma unroll
+        for (int k = 0; k < MAX_MEMBERS; ++k) om[k] = (k == am) ? T(1) : T(0);
+      } else {
+        T w[MAX_MEMBERS], tot = T(0);
+#pragma unroll
+        for (int k = 0; k < MAX_MEMBERS; ++k) {
+          w[k] = T(0);
+          if (k < nm) {
+            const T sg = (T)P.mem[k].sigma;
+            w[k] = apow<T>(d2[k], C<T>(-0.5)) *
+                   M<T>::exp(-d2[k] / (C<T>(2.0 * a.dim) * (sg * sg)));
+            tot = tot + w[k];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < MAX_MEMBERS; ++k)
+          if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;
+      }
+      // composition.py:157-166: zero weights are skipped
+      T total = T(0);
+#pragma unroll 1
+      for (int k = 0; k < nm; ++k) {
+        T omk = T(0);
+#pragma unroll
+        for (int kk = 0; kk < MAX_MEMBERS; ++kk)
+          if (kk == k) omk = om[kk];
+        const bool use = valid && omk != T(0);
+        if (!__syncthreads_or(use)) continue;
+        const rb_member& mem = P.mem[k];
+        const T g = member_value<T, GENERIC>(a, s, mem, use);
+        if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
+      }
+      result = total;
+    }
+    if (l8 == 0 && valid) a.f[row0 + p] = result + C<T>(100.0);     // engine.py:209
+    __syncthreads();                                                 // XS reused by next TMA
+  }
+}
+
+// Host-visible table of instantiations: [0..20] basic kernels, [21] generic.
+constexpr int N_VARIANTS = K_COUNT + 1;
+
+}  // namespace rb

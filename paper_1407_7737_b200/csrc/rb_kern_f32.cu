@@ -1,0 +1,22 @@
+// Instantiations of the evaluation kernel for float: one per basic kernel
+// (single-segment functions 0..22) plus the generic hybrid/composition
+// variant.  Compiled as its own unit so the build parallelises.
+#include "rb_device.cuh"
+
+namespace rb {
+
+extern const void* const kernels_f32[N_VARIANTS] = {
+    (const void*)evaluate_kernel<float, 0>,  (const void*)evaluate_kernel<float, 1>,
+    (const void*)evaluate_kernel<float, 2>,  (const void*)evaluate_kernel<float, 3>,
+    (const void*)evaluate_kernel<float, 4>,  (const void*)evaluate_kernel<float, 5>,
+    (const void*)evaluate_kernel<float, 6>,  (const void*)evaluate_kernel<float, 7>,
+    (const void*)evaluate_kernel<float, 8>,  (const void*)evaluate_kernel<float, 9>,
+    (const void*)evaluate_kernel<float, 10>, (const void*)evaluate_kernel<float, 11>,
+    (const void*)evaluate_kernel<float, 12>, (const void*)evaluate_kernel<float, 13>,
+    (const void*)evaluate_kernel<float, 14>, (const void*)evaluate_kernel<float, 15>,
+    (const void*)evaluate_kernel<float, 16>, (const void*)evaluate_kernel<float, 17>,
+    (const void*)evaluate_kernel<float, 18>, (const void*)evaluate_kernel<float, 19>,
+    (const void*)evaluate_kernel<float, 20>, (const void*)evaluate_kernel<float, GENERIC>,
+};
+
+}  // namespace rb

@@ -1,0 +1,22 @@
+// Instantiations of the evaluation kernel for double: one per basic kernel
+// (single-segment functions 0..22) plus the generic hybrid/composition
+// variant.  Compiled as its own unit so the build parallelises.
+#include "rb_device.cuh"
+
+namespace rb {
+
+extern const void* const kernels_f64[N_VARIANTS] = {
+    (const void*)evaluate_kernel<double, 0>,  (const void*)evaluate_kernel<double, 1>,
+    (const void*)evaluate_kernel<double, 2>,  (const void*)evaluate_kernel<double, 3>,
+    (const void*)evaluate_kernel<double, 4>,  (const void*)evaluate_kernel<double, 5>,
+    (const void*)evaluate_kernel<double, 6>,  (const void*)evaluate_kernel<double, 7>,
+    (const void*)evaluate_kernel<double, 8>,  (const void*)evaluate_kernel<double, 9>,
+    (const void*)evaluate_kernel<double, 10>, (const void*)evaluate_kernel<double, 11>,
+    (const void*)evaluate_kernel<double, 12>, (const void*)evaluate_kernel<double, 13>,
+    (const void*)evaluate_kernel<double, 14>, (const void*)evaluate_kernel<double, 15>,
+    (const void*)evaluate_kernel<double, 16>, (const void*)evaluate_kernel<double, 17>,
+    (const void*)evaluate_kernel<double, 18>, (const void*)evaluate_kernel<double, 19>,
+    (const void*)evaluate_kernel<double, 20>, (const void*)evaluate_kernel<double, GENERIC>,
+};
+
+}  // namespace rb

@@ -4,8 +4,13 @@
 // Each body restates the reference expression (line numbers below are
 // /root/reference/pkg/src/robench/kernels.py) with NumPy's evaluation order:
 // left-to-right binary ops, every product/sum individually rounded, Python
-// float constants rounded once into T, ``x**2`` on arrays = x*x, sums in the
-// pairwise order of rb::pw8, np.prod as a left fold.
+// float constants rounded once into T, ``x**2`` on arrays = x*x, array
+// powers through apow (NumPy's SVML powf in float32), sums in the pairwise
+// order of rb::pw8, np.prod as a left fold.
+//
+// kernel_value_k<T, K> is the compile-time specialisation used by the
+// per-function kernels; kernel_value<T>(k, ...) dispatches at run time for
+// hybrids and compositions.
 #pragma once
 #include "rb_math.cuh"
 
@@ -31,20 +36,20 @@ struct Pt {            // one point's view for the kernels
 
 template <class T> __device__ __forceinline__ T sq(T a) { return a * a; }
 
-// rosenbrock_pair (kernels.py:130-132): 100*(x*x - y)**2 + (x - 1)**2
+// rosenbrock_pair (:130-132): 100*(x*x - y)**2 + (x - 1)**2
 template <class T> __device__ __forceinline__ T rosen_link(T x, T y) {
   return C<T>(100.0) * sq(x * x - y) + sq(x - C<T>(1.0));
 }
-// griewank_1d (kernels.py:135-137): x*x/4000 - cos(x) + 1
+// griewank_1d (:135-137): x*x/4000 - cos(x) + 1
 template <class T> __device__ __forceinline__ T griewank_1d(T x) {
   return (x * x / C<T>(4000.0) - M<T>::cos(x)) + C<T>(1.0);
 }
-// schaffer_f6_pair (kernels.py:220-223)
+// schaffer_f6_pair (:220-223)
 template <class T> __device__ __forceinline__ T f6_link(T x, T y) {
   const T q = x * x + y * y;
   return (sq(M<T>::sin(M<T>::sqrt(q))) - C<T>(0.5)) / sq(C<T>(1.0) + C<T>(0.001) * q) + C<T>(0.5);
 }
-// schwefel_g1 (kernels.py:152-165): the branch np.where selects
+// schwefel_g1 (:152-165): the branch np.where selects
 template <class T> __device__ __forceinline__ T schwefel_g1(T w, T c10000d) {
   const T aw = M<T>::fabs(w);
   if (aw <= C<T>(500.0)) return w * M<T>::sin(M<T>::sqrt(aw));
@@ -56,137 +61,137 @@ template <class T> __device__ __forceinline__ T schwefel_g1(T w, T c10000d) {
   return (rem - C<T>(500.0)) * M<T>::sin(M<T>::sqrt(C<T>(500.0) - rem)) -
          sq(w + C<T>(500.0)) / c10000d;
 }
+// katsuura row sum over i = 1..32 (:178-180) for one coordinate: 8
+// accumulators in NumPy order (32 is a multiple of 8: no tail)
+template <class T> __device__ __forceinline__ T katsuura_row(T zj) {
+  T r[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) r[a] = T(0);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const T p2 = T(1ull << (i + 1));  // 2**(i+1), exact
+    const T w = p2 * zj;
+    r[i & 7] = r[i & 7] + M<T>::fabs(w - M<T>::floor(w + C<T>(0.5))) / p2;
+  }
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
+template <class T, int K>
+__device__ __forceinline__ T kernel_value_k(const Pt<T>& P) {
+  const T* z = P.z;
+  const int d = P.d, l8 = P.l8;
+  auto square = [&](int i) { const T a = z[i]; return a * a; };
+  if constexpr (K == K_SPHERE) {                                      // :52-54
+    return pw8<T>(0, d, square, l8);
+  } else if constexpr (K == K_ELLIPSOID) {                            // :57-60
+    return pw8<T>(0, d, [&](int i) { const T a = z[i]; return T(i + 1) * a * a; }, l8);
+  } else if constexpr (K == K_ELLIPTIC) {                             // :63-67
+    const T* c = P.ctab;
+    return pw8<T>(0, d, [&](int i) { const T a = z[i]; return c[i] * a * a; }, l8);
+  } else if constexpr (K == K_DISCUS) {                               // :70-72
+    const T rest = pw8<T>(1, d - 1, square, l8);
+    return C<T>(1.0e6) * z[0] * z[0] + rest;
+  } else if constexpr (K == K_CIGAR) {                                // :75-77
+    const T rest = pw8<T>(1, d - 1, square, l8);
+    return z[0] * z[0] + C<T>(1.0e6) * rest;
+  } else if constexpr (K == K_POWERS) {                               // :80-84
+    const T* e = P.ctab;
+    return M<T>::sqrt(pw8<T>(0, d, [&](int i) { return apow<T>(M<T>::fabs(z[i]), e[i]); }, l8));
+  } else if constexpr (K == K_SHARP_VALLEY) {                         // :87-89
+    const T rest = pw8<T>(1, d - 1, square, l8);
+    return z[0] * z[0] + C<T>(100.0) * M<T>::sqrt(rest);
+  } else if constexpr (K == K_STEP) {                                 // :92-95
+    return pw8<T>(0, d, [&](int i) { const T r = M<T>::floor(z[i] + C<T>(0.5)); return r * r; }, l8);
+  } else if constexpr (K == K_WEIERSTRASS) {                          // :98-106
+    // the flattened (d, 21) grid: element e = 21*j + k
+    const T* ak = P.ctab;
+    const T* arg = P.ctab + 21;
+    auto term = [&](int e) {
+      const int j = e / 21, kk = e - 21 * j;
+      return ak[kk] * M<T>::cos(arg[kk] * (z[j] + C<T>(0.5)));
+    };
+    return pw8<T>(0, 21 * d, term, l8) - P.ctab[42];
+  } else if constexpr (K == K_GRIEWANK) {                             // :109-112
+    const T s = pw8<T>(0, d, square, l8);
+    const T p = prod8<T>(d, [&](int i) { return M<T>::cos(z[i] / M<T>::sqrt(T(i + 1))); }, l8);
+    return (s / C<T>(4000.0) - p) + C<T>(1.0);
+  } else if constexpr (K == K_RASTRIGIN) {                            // :115-117
+    return pw8<T>(0, d, [&](int i) {
+      const T a = z[i];
+      return (a * a - C<T>(10.0) * M<T>::cos(C<T>(kTwoPi) * a)) + C<T>(10.0);
+    }, l8);
+  } else if constexpr (K == K_SCHAFFERS_F7) {                         // :120-127
+    if (d < 2) return T(0);
+    const T s = pw8<T>(0, d - 1, [&](int i) {
+      const T w = M<T>::sqrt(sq(z[i]) + sq(z[i + 1]));
+      return M<T>::sqrt(w) * (C<T>(1.0) + sq(M<T>::sin(C<T>(50.0) * apow<T>(w, C<T>(0.2)))));
+    }, l8);
+    return sq(s / T(d - 1));
+  } else if constexpr (K == K_GRIE_ROSEN) {                           // :140-142
+    return pw8<T>(0, d, [&](int i) {
+      const int n = (i + 1 == d) ? 0 : i + 1;
+      return griewank_1d(rosen_link(z[i], z[n]));
+    }, l8);
+  } else if constexpr (K == K_ROSENBROCK) {                           // :145-149
+    return pw8<T>(0, d - 1, [&](int i) { return rosen_link(z[i], z[i + 1]); }, l8);
+  } else if constexpr (K == K_SCHWEFEL) {                             // :168-171
+    const T c10000d = C<T>(10000.0 * d);
+    const T s = pw8<T>(0, d, [&](int i) {
+      return schwefel_g1(z[i] + C<T>(420.9687462275036), c10000d);
+    }, l8);
+    return C<T>(418.9829 * d) - s;
+  } else if constexpr (K == K_KATSUURA) {                             // :174-184
+    auto logt = [&](int j) { return M<T>::log(C<T>(1.0) + T(j + 1) * katsuura_row(z[j])); };
+    const T lp = P.ctab[0] * pw8<T>(0, d, logt, l8);
+    return P.ctab[1] * M<T>::expm1(lp);
+  } else if constexpr (K == K_LUNACEK) {                              // :187-193
+    const T s1 = pw8<T>(0, d, [&](int i) { const T a = z[i] - C<T>(2.5); return a * a; }, l8);
+    const T s2 = pw8<T>(0, d, [&](int i) { const T b = z[i] - C<T>(-2.5); return b * b; }, l8);
+    const T cs = pw8<T>(0, d, [&](int i) {
+      return M<T>::cos(C<T>(kTwoPi) * (z[i] - C<T>(2.5)));
+    }, l8);
+    const T alt = C<T>(1.0 * d) + C<T>(0.9) * s2;
+    const T funnel = (alt < s1) ? alt : s1;   // np.minimum (finite operands)
+    return funnel + C<T>(10.0) * (T(d) - cs);
+  } else if constexpr (K == K_ACKLEY) {                               // :196-201
+    const T s = pw8<T>(0, d, square, l8);
+    const T cs = pw8<T>(0, d, [&](int i) { return M<T>::cos(C<T>(kTwoPi) * z[i]); }, l8);
+    const T rms = M<T>::sqrt(s / T(d));
+    const T mc = cs / T(d);
+    return ((C<T>(-20.0) * M<T>::exp(C<T>(-0.2) * rms) - M<T>::exp(mc)) + C<T>(20.0)) + C<T>(kE);
+  } else if constexpr (K == K_HAPPYCAT) {                             // :204-209
+    const T r2 = pw8<T>(0, d, square, l8);
+    const T sz = pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
+    return (M<T>::pow(M<T>::fabs(r2 - T(d)), C<T>(0.25)) + (C<T>(0.5) * r2 + sz) / T(d)) +
+           C<T>(0.5);
+  } else if constexpr (K == K_HGBAT) {                                // :212-217
+    const T r2 = pw8<T>(0, d, square, l8);
+    const T sz = pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
+    return (M<T>::sqrt(M<T>::fabs(r2 * r2 - sz * sz)) + (C<T>(0.5) * r2 + sz) / T(d)) +
+           C<T>(0.5);
+  } else if constexpr (K == K_SCHAFFERS_F6) {                         // :226-228
+    return pw8<T>(0, d, [&](int i) {
+      const int n = (i + 1 == d) ? 0 : i + 1;
+      return f6_link(z[i], z[n]);
+    }, l8);
+  } else {
+    return T(0);
+  }
+}
 
 template <class T>
 __device__ T kernel_value(int k, const Pt<T>& P) {
-  const T* z = P.z;
-  const int d = P.d, l8 = P.l8;
   switch (k) {
-    case K_SPHERE:                                                     // :52-54
-      return pw8<T>(0, d, [&](int i) { const T a = z[i]; return a * a; }, l8);
-    case K_ELLIPSOID:                                                  // :57-60
-      return pw8<T>(0, d, [&](int i) { const T a = z[i]; return T(i + 1) * a * a; }, l8);
-    case K_ELLIPTIC: {                                                 // :63-67
-      const T* c = P.ctab;
-      return pw8<T>(0, d, [&](int i) { const T a = z[i]; return c[i] * a * a; }, l8);
-    }
-    case K_DISCUS: {                                                   // :70-72
-      const T rest = pw8<T>(1, d - 1, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      return C<T>(1.0e6) * z[0] * z[0] + rest;
-    }
-    case K_CIGAR: {                                                    // :75-77
-      const T rest = pw8<T>(1, d - 1, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      return z[0] * z[0] + C<T>(1.0e6) * rest;
-    }
-    case K_POWERS: {                                                   // :80-84
-      const T* e = P.ctab;
-      return M<T>::sqrt(pw8<T>(0, d, [&](int i) { return apow<T>(M<T>::fabs(z[i]), e[i]); }, l8));
-    }
-    case K_SHARP_VALLEY: {                                             // :87-89
-      const T rest = pw8<T>(1, d - 1, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      return z[0] * z[0] + C<T>(100.0) * M<T>::sqrt(rest);
-    }
-    case K_STEP:                                                       // :92-95
-      return pw8<T>(0, d, [&](int i) { const T r = M<T>::floor(z[i] + C<T>(0.5)); return r * r; }, l8);
-    case K_WEIERSTRASS: {                                              // :98-106
-      // flattened (d, 21) grid: element e = 21*j + k
-      const T* ak = P.ctab;
-      const T* arg = P.ctab + 21;
-      const T dbase = P.ctab[42];
-      auto term = [&](int e) {
-        const int j = e / 21, kk = e - 21 * j;
-        return ak[kk] * M<T>::cos(arg[kk] * (z[j] + C<T>(0.5)));
-      };
-      return pw8<T>(0, 21 * d, term, l8) - dbase;
-    }
-    case K_GRIEWANK: {                                                 // :109-112
-      const T s = pw8<T>(0, d, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      const T p = prod8<T>(d, [&](int i) { return M<T>::cos(z[i] / M<T>::sqrt(T(i + 1))); }, l8);
-      return (s / C<T>(4000.0) - p) + C<T>(1.0);
-    }
-    case K_RASTRIGIN:                                                  // :115-117
-      return pw8<T>(0, d, [&](int i) {
-        const T a = z[i];
-        return (a * a - C<T>(10.0) * M<T>::cos(C<T>(kTwoPi) * a)) + C<T>(10.0);
-      }, l8);
-    case K_SCHAFFERS_F7: {                                             // :120-127
-      if (d < 2) return T(0);
-      const T s = pw8<T>(0, d - 1, [&](int i) {
-        const T w = M<T>::sqrt(sq(z[i]) + sq(z[i + 1]));
-        return M<T>::sqrt(w) * (C<T>(1.0) + sq(M<T>::sin(C<T>(50.0) * apow<T>(w, C<T>(0.2)))));
-      }, l8);
-      return sq(s / T(d - 1));
-    }
-    case K_GRIE_ROSEN:                                                 // :140-142
-      return pw8<T>(0, d, [&](int i) {
-        const int n = (i + 1 == d) ? 0 : i + 1;
-        return griewank_1d(rosen_link(z[i], z[n]));
-      }, l8);
-    case K_ROSENBROCK:                                                 // :145-149
-      return pw8<T>(0, d - 1, [&](int i) { return rosen_link(z[i], z[i + 1]); }, l8);
-    case K_SCHWEFEL: {                                                 // :168-171
-      const T c10000d = C<T>(10000.0 * d);
-      const T s = pw8<T>(0, d, [&](int i) {
-        return schwefel_g1(z[i] + C<T>(420.9687462275036), c10000d);
-      }, l8);
-      return C<T>(418.9829 * d) - s;
-    }
-    case K_KATSUURA: {                                                 // :174-184
-      // lane owning coordinate j sums its 32 terms itself (8 accumulators,
-      // NumPy order; 32 is a multiple of 8 so there is no tail)
-      auto logt = [&](int j) {
-        const T zj = z[j];
-        T r[8];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) r[a] = T(0);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const T p2 = T(1ull << (i + 1));  // 2**(i+1), exact
-          const T w = p2 * zj;
-          r[i & 7] = r[i & 7] + M<T>::fabs(w - M<T>::floor(w + C<T>(0.5))) / p2;
-        }
-        const T s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        return M<T>::log(C<T>(1.0) + T(j + 1) * s);
-      };
-      const T lp = P.ctab[0] * pw8<T>(0, d, logt, l8);
-      return P.ctab[1] * M<T>::expm1(lp);
-    }
-    case K_LUNACEK: {                                                  // :187-193
-      const T s1 = pw8<T>(0, d, [&](int i) { const T a = z[i] - C<T>(2.5); return a * a; }, l8);
-      const T s2 = pw8<T>(0, d, [&](int i) { const T b = z[i] - C<T>(-2.5); return b * b; }, l8);
-      const T cs = pw8<T>(0, d, [&](int i) {
-        return M<T>::cos(C<T>(kTwoPi) * (z[i] - C<T>(2.5)));
-      }, l8);
-      const T alt = C<T>(1.0 * d) + C<T>(0.9) * s2;
-      const T funnel = (alt < s1) ? alt : s1;   // np.minimum (finite operands)
-      return funnel + C<T>(10.0) * (T(d) - cs);
-    }
-    case K_ACKLEY: {                                                   // :196-201
-      const T s = pw8<T>(0, d, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      const T cs = pw8<T>(0, d, [&](int i) { return M<T>::cos(C<T>(kTwoPi) * z[i]); }, l8);
-      const T rms = M<T>::sqrt(s / T(d));
-      const T mc = cs / T(d);
-      return ((C<T>(-20.0) * M<T>::exp(C<T>(-0.2) * rms) - M<T>::exp(mc)) + C<T>(20.0)) + C<T>(kE);
-    }
-    case K_HAPPYCAT: {                                                 // :204-209
-      const T r2 = pw8<T>(0, d, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      const T sz = pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
-      return (M<T>::pow(M<T>::fabs(r2 - T(d)), C<T>(0.25)) + (C<T>(0.5) * r2 + sz) / T(d)) +
-             C<T>(0.5);
-    }
-    case K_HGBAT: {                                                    // :212-217
-      const T r2 = pw8<T>(0, d, [&](int i) { const T a = z[i]; return a * a; }, l8);
-      const T sz = pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
-      return (M<T>::sqrt(M<T>::fabs(r2 * r2 - sz * sz)) + (C<T>(0.5) * r2 + sz) / T(d)) +
-             C<T>(0.5);
-    }
-    case K_SCHAFFERS_F6:                                               // :226-228
-      return pw8<T>(0, d, [&](int i) {
-        const int n = (i + 1 == d) ? 0 : i + 1;
-        return f6_link(z[i], z[n]);
-      }, l8);
-    default:
-      return T(0);
+#define RB_CASE(K) \
+  case K: return kernel_value_k<T, K>(P);
+    RB_CASE(K_SPHERE) RB_CASE(K_ELLIPSOID) RB_CASE(K_ELLIPTIC) RB_CASE(K_DISCUS)
+    RB_CASE(K_CIGAR) RB_CASE(K_POWERS) RB_CASE(K_SHARP_VALLEY) RB_CASE(K_STEP)
+    RB_CASE(K_WEIERSTRASS) RB_CASE(K_GRIEWANK) RB_CASE(K_RASTRIGIN) RB_CASE(K_SCHAFFERS_F7)
+    RB_CASE(K_GRIE_ROSEN) RB_CASE(K_ROSENBROCK) RB_CASE(K_SCHWEFEL) RB_CASE(K_KATSUURA)
+    RB_CASE(K_LUNACEK) RB_CASE(K_ACKLEY) RB_CASE(K_HAPPYCAT) RB_CASE(K_HGBAT)
+    RB_CASE(K_SCHAFFERS_F6)
+#undef RB_CASE
+    default: return T(0);
   }
 }
 

@@ -8,21 +8,23 @@
 #include <stdint.h>
 
 #include "rb_svml_powf.cuh"
+#include "rb_trig.cuh"
 
 #define RB_FULL 0xffffffffu
 
 namespace rb {
 
 // ---------------------------------------------------------------- math
-// float64: CUDA's double libm (<= 2 ulp).  float32: evaluated in double and
-// rounded once, i.e. (almost always) the correctly rounded float result;
-// NumPy's float32 SIMD transcendentals are within ~1-2 ulp of that
-// (measured on the box).
+// float64: CUDA's double libm (<= 2 ulp), sin/cos through rb_trig.cuh (no
+// Payne-Hanek slow path).  float32: evaluated in double and rounded once,
+// i.e. (almost always) the correctly rounded float result; NumPy's float32
+// SIMD transcendentals are within ~1-2 ulp of that (DESIGN.md "float32
+// transcendentals").
 template <class T> struct M;
 
 template <> struct M<double> {
-  static __device__ __forceinline__ double cos(double x) { return ::cos(x); }
-  static __device__ __forceinline__ double sin(double x) { return ::sin(x); }
+  static __device__ __forceinline__ double cos(double x) { return fast_cos(x); }
+  static __device__ __forceinline__ double sin(double x) { return fast_sin(x); }
   static __device__ __forceinline__ double exp(double x) { return ::exp(x); }
   static __device__ __forceinline__ double log(double x) { return ::log(x); }
   static __device__ __forceinline__ double expm1(double x) { return ::expm1(x); }
@@ -35,8 +37,8 @@ template <> struct M<double> {
 };
 
 template <> struct M<float> {
-  static __device__ __forceinline__ float cos(float x) { return (float)::cos((double)x); }
-  static __device__ __forceinline__ float sin(float x) { return (float)::sin((double)x); }
+  static __device__ __forceinline__ float cos(float x) { return (float)fast_cos((double)x); }
+  static __device__ __forceinline__ float sin(float x) { return (float)fast_sin((double)x); }
   static __device__ __forceinline__ float exp(float x) { return (float)::exp((double)x); }
   static __device__ __forceinline__ float log(float x) { return (float)::log((double)x); }
   static __device__ __forceinline__ float expm1(float x) { return (float)::expm1((double)x); }

@@ -30,7 +30,7 @@ import numpy as np
 from . import catalog, instances
 
 GROUP_DT = np.dtype([("m", "<i4"), ("qb", "<i4", (10,)), ("col", "<i4"),
-                     ("row", "<i4"), ("mat", "<i4")])
+                     ("row", "<i4"), ("mat", "<i4"), ("frag", "<i4"), ("reserved", "<i4")])
 SEGMENT_DT = np.dtype({
     "names": ["kernel", "d", "src", "n_groups", "group0", "ctab", "scale", "pre", "post"],
     "formats": ["<i4"] * 6 + ["<f8"] * 3,
@@ -90,10 +90,16 @@ class _Builder:
 
     # -- tables
     def values(self, a64, a32=None) -> int:
+        """Append to both value tables; every block starts 32-byte aligned."""
         a64 = np.ascontiguousarray(a64, dtype=np.float64).ravel()
         a32 = (a64.astype(np.float32) if a32 is None
                else np.ascontiguousarray(a32, dtype=np.float32).ravel())
         assert a64.shape == a32.shape
+        if self.n_values % 4:
+            pad = 4 - self.n_values % 4
+            self.v64.append(np.zeros(pad))
+            self.v32.append(np.zeros(pad, np.float32))
+            self.n_values += pad
         off = self.n_values
         self.v64.append(a64)
         self.v32.append(a32)
@@ -118,12 +124,20 @@ class _Builder:
         qb = np.searchsorted(np.asarray(slots), np.arange(10), side="left").astype(np.int32)
         qb[9] = m
         mat = np.ascontiguousarray(block[:, order].T)          # mat[q, r] = block[r, order[q]]
+        m4, nt, nk = (m + 3) // 4 * 4, (m + 7) // 8, (m + 3) // 4
+        padded = np.zeros((nk * 4, nt * 8))
+        padded[:m, :m] = mat
+        lane = np.arange(32)
+        # frag[nt][ks][lane] = padded[4ks + lane%4, 8nt + lane/4]
+        frag = padded[(4 * np.arange(nk)[None, :, None] + lane % 4)[..., :],
+                      (8 * np.arange(nt)[:, None, None] + lane // 4)]
         rec = np.zeros((), dtype=GROUP_DT)
         rec["m"] = m
         rec["qb"] = qb
         rec["col"] = self.ints([cols[k] for k in order])
         rec["row"] = self.ints(rows)
-        rec["mat"] = self.values(mat)
+        rec["mat"] = self.values(padded[:m, :m4])
+        rec["frag"] = self.values(frag)
         self.groups.append(rec)
         return len(self.groups) - 1
 

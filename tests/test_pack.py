@@ -16,7 +16,8 @@ def exact_order_rotate(pk, group, v):
     qb = group["qb"]
     cols = pk.index[group["col"]:group["col"] + m]
     rows = pk.index[group["row"]:group["row"] + m]
-    mat = pk.values_f32[group["mat"]:group["mat"] + m * m].reshape(m, m)
+    m4 = (m + 3) // 4 * 4                      # rows 4-padded (float4 loads)
+    mat = pk.values_f32[group["mat"]:group["mat"] + m * m4].reshape(m, m4)
     out = {}
     for r in range(m):
         t0 = t1 = t2 = F32(0)
@@ -90,6 +91,22 @@ def test_pack_shapes_and_disabled():
     sizes = [int(pk100.groups[seg["group0"] + g]["m"]) for g in range(seg["n_groups"])]
     assert sizes == [34, 33, 33]
     assert pk100.max_exact_len == 100
+
+
+def test_dmma_fragments_match_q_ordered_block():
+    pk = P.Pack(100, 0)
+    for g in pk.groups[:6]:
+        m = int(g["m"])
+        nt, nk, m4 = (m + 7) // 8, (m + 3) // 4, (m + 3) // 4 * 4
+        mat = pk.values_f64[g["mat"]:g["mat"] + m * m4].reshape(m, m4)
+        frag = pk.values_f64[g["frag"]:g["frag"] + nt * nk * 32].reshape(nt, nk, 32)
+        for a in range(nt):
+            for ks in range(nk):
+                for lane in range(32):
+                    q, r = 4 * ks + lane % 4, 8 * a + lane // 4
+                    want = mat[q, r] if (q < m and r < m) else 0.0
+                    assert frag[a, ks, lane] == want
+        assert g["mat"] % 4 == 0 and g["frag"] % 4 == 0
 
 
 def test_kernel_constants_follow_numpy():
