@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <mutex>
@@ -61,7 +62,15 @@ struct Launch {
   size_t smem = 0;
   int grid_cap = 0;
   int ldv = 0, max_q = 0;
+  int nbuf = 1;
+  size_t smem_nbuf[3] = {0, 0, 0};
 };
+
+// RB_PREFETCH=0/1 forces single / double X buffering (default: auto).
+int prefetch_mode() {
+  const char* v = std::getenv("RB_PREFETCH");
+  return v ? std::atoi(v) : -1;
+}
 
 }  // namespace
 
@@ -155,6 +164,7 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   a.ldv = L.ldv;
   a.max_q = L.max_q;
   a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+  a.nbuf = L.nbuf;
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
   void* args[] = {&a};
@@ -244,11 +254,13 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       L.func = (pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[variant[fi]];
       L.max_q = std::max(max_q, 1);
       L.ldv = ldv;
-      L.smem = pi == 0 ? rb::smem_bytes<double>(pk->dim, ldv, e->ldz[0], L.max_q)
-                       : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q);
-      if ((int)L.smem > optin)
+      for (int nb = 1; nb <= 2; ++nb)
+        L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, ldv, e->ldz[0], L.max_q, nb)
+                                  : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q, nb);
+      if ((int)L.smem_nbuf[1] > optin)
         return fail(RB_E_UNSUPPORTED, "dimension too large for the shared-memory tile");
-      need[pi][variant[fi]] = std::max(need[pi][variant[fi]], L.smem);
+      const size_t top = (int)L.smem_nbuf[2] <= optin ? L.smem_nbuf[2] : L.smem_nbuf[1];
+      need[pi][variant[fi]] = std::max(need[pi][variant[fi]], top);
     }
   }
   for (int pi = 0; pi < 2; ++pi)
@@ -260,10 +272,16 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
     if (pk->functions[fi].category == RB_DISABLED) continue;
     for (int pi = 0; pi < 2; ++pi) {
       Launch& L = e->launch[pi][fi];
-      int per_sm = 0;
-      RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.func, rb::NT, L.smem));
-      if (per_sm < 1) return fail(RB_E_UNSUPPORTED, "kernel does not fit on an SM");
-      L.grid_cap = sms * per_sm;
+      int occ[3] = {0, 0, 0};
+      for (int nb = 1; nb <= 2; ++nb)
+        if ((int)L.smem_nbuf[nb] <= optin)
+          RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[nb], L.func, rb::NT,
+                                                                L.smem_nbuf[nb]));
+      if (occ[1] < 1) return fail(RB_E_UNSUPPORTED, "kernel does not fit on an SM");
+      const int mode = prefetch_mode();
+      L.nbuf = (mode == 1 && occ[2] >= 1) || (mode < 0 && occ[2] >= 2 && occ[2] >= occ[1] - 1) ? 2 : 1;
+      L.smem = L.smem_nbuf[L.nbuf];
+      L.grid_cap = sms * occ[L.nbuf];
     }
   }
   return RB_OK;

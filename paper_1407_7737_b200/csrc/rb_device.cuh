@@ -50,6 +50,7 @@ struct Args {
   int ldv;          // fp32 V tile rows (sum of 4-padded group sizes)
   int max_q;        // capacity of the plan's gather tables
   int tma;          // x is 16-byte aligned: bulk-copy full tiles
+  int nbuf;         // 2: prefetch the next tile while computing this one
 };
 
 struct PlanHead {
@@ -59,16 +60,17 @@ struct PlanHead {
   rb_segment seg[MAX_SEGMENTS];
   rb_group grp[MAX_GROUPS];
   int gq0[MAX_GROUPS];            // group g's slice of the gather tables
-  unsigned long long mbar;        // TMA completion barrier
+  unsigned long long mbar[2];     // TMA completion barriers, one per X buffer
 };
 
-// dynamic shared memory: [PlanHead][qsrc int[max_q]][qo T[max_q]][XS][V][ZS]
+// dynamic shared memory: [PlanHead][qsrc int[max_q]][qo T[max_q]][XB0 (XB1)][V][ZS]
 template <class T>
 struct Smem {
   PlanHead* P;
   int* qsrc;      // x column feeding the group's q-th column (split perm applied)
   T* qo;          // the optimum at that column
-  T* XS;          // [TP][dim]
+  T* XS;          // [TP][dim], the current tile (one of XB)
+  T* XB[2];       // X tile buffers (XB[1] == XB[0] without prefetch)
   T* VS;          // fp32 only: [ldv][TP]
   T* ZS;          // [TP][ldz]
 };
@@ -76,10 +78,10 @@ struct Smem {
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
 template <class T>
-__host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q) {
+__host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q, int nbuf) {
   size_t b = align16(sizeof(PlanHead));
   b += align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
-  b += align16(sizeof(T) * TP * dim);
+  b += nbuf * align16(sizeof(T) * TP * dim);
   if (sizeof(T) == 4) b += align16(sizeof(T) * TP * ldv);
   b += align16(sizeof(T) * TP * ldz);
   return b;
@@ -95,8 +97,14 @@ __device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
   off += align16(sizeof(int) * a.max_q);
   s.qo = reinterpret_cast<T*>(base + off);
   off += align16(sizeof(T) * a.max_q);
-  s.XS = reinterpret_cast<T*>(base + off);
+  s.XB[0] = reinterpret_cast<T*>(base + off);
   off += align16(sizeof(T) * TP * a.dim);
+  s.XB[1] = s.XB[0];
+  if (a.nbuf == 2) {
+    s.XB[1] = reinterpret_cast<T*>(base + off);
+    off += align16(sizeof(T) * TP * a.dim);
+  }
+  s.XS = s.XB[0];
   s.VS = reinterpret_cast<T*>(base + off);
   if (sizeof(T) == 4) off += align16(sizeof(T) * TP * a.ldv);
   s.ZS = reinterpret_cast<T*>(base + off);
@@ -125,7 +133,8 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
     const rb_segment sl = a.segments[last.segment0 + last.n_segments - 1];
     P.grp_base = s0.group0;
     P.n_grp = sl.group0 + sl.n_groups - s0.group0;
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -164,42 +173,44 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
 }
 
 // ------------------------------------------------------------- X tile load
+// A tile is 32 consecutive rows = one contiguous span of X, so one
+// cp.async.bulk (TMA bulk copy, completion on an mbarrier) moves it.
 template <class T>
-__device__ void load_tile(const Args<T>& a, const Smem<T>& s, int64_t row0, int nv,
-                          uint32_t& phase) {
-  const int D = a.dim;
-  const uint32_t bytes = (uint32_t)(sizeof(T) * (size_t)nv * D);
-  const T* src = a.x + row0 * D;
-  if (a.tma && (bytes & 15u) == 0) {
-    if (threadIdx.x == 0) {
-      const uint32_t bar = smem_u32(&s.P->mbar);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(s.XS)),
-          "l"(src), "r"(bytes), "r"(bar)
-          : "memory");
-    }
-    const uint32_t bar = smem_u32(&s.P->mbar);
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(bar), "r"(phase)
-          : "memory");
-    }
-    phase ^= 1u;
-  } else {
-    for (int e = threadIdx.x; e < nv * D; e += NT) s.XS[e] = src[e];
-    __syncthreads();
+__device__ __forceinline__ bool tile_is_bulk(const Args<T>& a, int nv) {
+  return a.tma && ((sizeof(T) * (size_t)nv * a.dim) & 15u) == 0;
+}
+
+template <class T>
+__device__ __forceinline__ int tile_rows(const Args<T>& a, int64_t tile) {
+  const int64_t left = a.n - tile * TP;
+  return left < TP ? (int)left : TP;
+}
+
+// thread 0 only
+template <class T>
+__device__ __forceinline__ void issue_tile(const Args<T>& a, T* dst, unsigned long long* mbar,
+                                           int64_t tile, int nv) {
+  const uint32_t bytes = (uint32_t)(sizeof(T) * (size_t)nv * a.dim);
+  const uint32_t bar = smem_u32(mbar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(a.x + tile * TP * a.dim), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void wait_tile(unsigned long long* mbar, uint32_t phase) {
+  const uint32_t bar = smem_u32(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
   }
-  // finiteness of the batch (engine.py:202-203)
-  bool bad = false;
-  for (int e = threadIdx.x; e < nv * D; e += NT) bad |= !M<T>::finite(s.XS[e]);
-  if (bad) atomicOr(a.flag, 1);
 }
 
 // ------------------------------------------------------------ rotate fp64
@@ -250,6 +261,7 @@ __device__ inline void rotate(const Args<double>& a, const Smem<double>& s, cons
     for (int c = 0; c < NTC; ++c)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[c][i] = 0.0;
+#pragma unroll 2
     for (int ks = 0; ks < nks; ++ks) {
       const int q = ks * 4 + tig;
       double a0 = 0.0, a1 = 0.0;
@@ -443,24 +455,54 @@ __global__ void __launch_bounds__(NT, 2) evaluate_kernel(const Args<T> a) {
   const PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  uint32_t phase = 0;
+  uint32_t phase0 = 0u, phase1 = 0u;
+  const int64_t first = blockIdx.x;
+  if (a.nbuf == 2 && threadIdx.x == 0 && first < ntiles && tile_is_bulk(a, tile_rows(a, first)))
+    issue_tile(a, s.XB[0], &s.P->mbar[0], first, tile_rows(a, first));
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int it = 0;
+  for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = (a.nbuf == 2) ? (it & 1) : 0;
+    Smem<T> st = s;
+    st.XS = b ? s.XB[1] : s.XB[0];
     const int64_t row0 = tile * TP;
-    const int64_t left = a.n - row0;
-    const int nv = left < TP ? (int)left : TP;
-    load_tile(a, s, row0, nv, phase);
+    const int nv = tile_rows(a, tile);
+    const int64_t next = tile + gridDim.x;
+    if (threadIdx.x == 0) {
+      if (a.nbuf == 2 && next < ntiles && tile_is_bulk(a, tile_rows(a, next)))
+        issue_tile(a, b ? s.XB[0] : s.XB[1], b ? &s.P->mbar[0] : &s.P->mbar[1], next,
+                   tile_rows(a, next));
+      if (a.nbuf == 1 && tile_is_bulk(a, nv)) issue_tile(a, st.XS, &s.P->mbar[0], tile, nv);
+    }
+    if (tile_is_bulk(a, nv)) {
+      if (b) {
+        wait_tile(&s.P->mbar[1], phase1);
+        phase1 ^= 1u;
+      } else {
+        wait_tile(&s.P->mbar[0], phase0);
+        phase0 ^= 1u;
+      }
+    } else {
+      const T* src = a.x + row0 * a.dim;
+      for (int e = threadIdx.x; e < nv * a.dim; e += NT) st.XS[e] = src[e];
+      __syncthreads();
+    }
+    {                                                     // engine.py:202-203
+      bool bad = false;
+      for (int e = threadIdx.x; e < nv * a.dim; e += NT) bad |= !M<T>::finite(st.XS[e]);
+      if (bad) atomicOr(a.flag, 1);
+    }
     __syncthreads();
     const bool valid = p < nv;
     T result;
     if constexpr (KID >= 0) {
-      result = member_value<T, KID>(a, s, P.mem[0], valid);
+      result = member_value<T, KID>(a, st, P.mem[0], valid);
     } else if (P.fn.category != RB_COMPOSITION) {
-      result = member_value<T, GENERIC>(a, s, P.mem[0], valid);
+      result = member_value<T, GENERIC>(a, st, P.mem[0], valid);
     } else {
       // composition.py:114-141: weights from the squared distances
       const int nm = P.fn.n_members;
-      const T* x = s.XS + p * a.dim;
+      const T* x = st.XS + p * a.dim;
       T d2[MAX_MEMBERS], om[MAX_MEMBERS];
 #pragma unroll
       for (int k = 0; k < MAX_MEMBERS; ++k) {
@@ -506,7 +548,7 @@ __global__ void __launch_bounds__(NT, 2) evaluate_kernel(const Args<T> a) {
         const bool use = valid && omk != T(0);
         if (!__syncthreads_or(use)) continue;
         const rb_member& mem = P.mem[k];
-        const T g = member_value<T, GENERIC>(a, s, mem, use);
+        const T g = member_value<T, GENERIC>(a, st, mem, use);
         if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
       }
       result = total;
