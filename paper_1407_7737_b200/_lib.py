@@ -14,7 +14,9 @@ import numpy as np
 
 from . import errors, pack
 
-LIB_PATH = Path(__file__).resolve().with_name("librobench_b200.so")
+import os
+
+LIB_PATH = Path(os.environ.get("RB_LIB") or Path(__file__).resolve().with_name("librobench_b200.so"))
 
 RB_OK = 0
 _STATUS = {

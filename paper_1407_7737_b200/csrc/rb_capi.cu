@@ -279,7 +279,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
                                                                 L.smem_nbuf[nb]));
       if (occ[1] < 1) return fail(RB_E_UNSUPPORTED, "kernel does not fit on an SM");
       const int mode = prefetch_mode();
-      L.nbuf = (mode == 1 && occ[2] >= 1) || (mode < 0 && occ[2] >= 2 && occ[2] >= occ[1] - 1) ? 2 : 1;
+      L.nbuf = (mode == 1 && occ[2] >= 1) || (mode < 0 && occ[2] >= occ[1]) ? 2 : 1;
       L.smem = L.smem_nbuf[L.nbuf];
       L.grid_cap = sms * occ[L.nbuf];
     }

@@ -29,7 +29,19 @@ constexpr int NT = 256;         // threads per CTA = 8 lanes x TP
 constexpr int MAX_MEMBERS = 5;
 constexpr int MAX_SEGMENTS = 16;
 constexpr int MAX_GROUPS = 16;
-constexpr int NTC = 5;          // DMMA n-tiles (8 rows) per warp strip
+#ifndef RB_NTC
+#define RB_NTC 2
+#endif
+#ifndef RB_MIN_BLOCKS_F64
+#define RB_MIN_BLOCKS_F64 3
+#endif
+#ifndef RB_MIN_BLOCKS_F32
+#define RB_MIN_BLOCKS_F32 2
+#endif
+#ifndef RB_F32_ROWS
+#define RB_F32_ROWS 4             // rows per pass of the float32 rotate tile (4 or 2)
+#endif
+constexpr int NTC = RB_NTC;     // DMMA n-tiles (8 rows) per warp strip
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
 template <class T>
@@ -336,62 +348,74 @@ __device__ inline void rotate(const Args<float>& a, const Smem<float>& s, const 
     const rb_group& G = P.grp[g];
     const int pq = rem & 7, rq = rem >> 3;
     const int m = G.m, m4 = round4(m);
-    const float* B = a.values + G.mat + rq * 4;
-    float t0[4][4], t1[4][4], t2[4][4], acc[4][4];
+    constexpr int RR = RB_F32_ROWS;
+#pragma unroll 1
+    for (int pass = 0; pass < 4 / RR; ++pass) {
+      const int r0 = rq * 4 + pass * RR;
+      if (r0 >= m) break;
+      const float* B = a.values + G.mat + r0;
+      float t0[4][RR], t1[4][RR], t2[4][RR], acc[4][RR];
 #pragma unroll
-    for (int sl = 0; sl < 8; ++sl) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-      for (int q = G.qb[sl]; q < G.qb[sl + 1]; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
-        const float4 b = __ldg(reinterpret_cast<const float4*>(B + q * m4));
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        const float bb[4] = {b.x, b.y, b.z, b.w};
+      for (int sl = 0; sl < 8; ++sl) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(vv[i], bb[j]));
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float x = acc[i][j];
-          switch (sl) {
-            case 0: t0[i][j] = x; break;
-            case 1: t0[i][j] = __fadd_rn(t0[i][j], x); break;
-            case 2: t1[i][j] = x; break;
-            case 3: t1[i][j] = __fadd_rn(t1[i][j], x); t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]); break;
-            case 4: t1[i][j] = x; break;
-            case 5: t1[i][j] = __fadd_rn(t1[i][j], x); break;
-            case 6: t2[i][j] = x; break;
-            default:
-              t2[i][j] = __fadd_rn(t2[i][j], x);
-              t1[i][j] = __fadd_rn(t1[i][j], t2[i][j]);
-              t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]);
+          for (int j = 0; j < RR; ++j) acc[i][j] = 0.0f;
+        for (int q = G.qb[sl]; q < G.qb[sl + 1]; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
+          float bb[RR];
+          if constexpr (RR == 4) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(B + q * m4));
+            bb[0] = b.x; bb[1] = b.y; bb[2] = b.z; bb[3] = b.w;
+          } else {
+            const float2 b = __ldg(reinterpret_cast<const float2*>(B + q * m4));
+            bb[0] = b.x; bb[1] = b.y;
           }
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < RR; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(vv[i], bb[j]));
         }
-    }
-    for (int q = G.qb[8]; q < G.qb[9]; ++q) {
-      const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
-      const float4 b = __ldg(reinterpret_cast<const float4*>(B + q * m4));
-      const float vv[4] = {v.x, v.y, v.z, v.w};
-      const float bb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], bb[j]));
-    }
-    const int32_t* rows = a.index + G.row;
+          for (int j = 0; j < RR; ++j) {
+            const float x = acc[i][j];
+            switch (sl) {
+              case 0: t0[i][j] = x; break;
+              case 1: t0[i][j] = __fadd_rn(t0[i][j], x); break;
+              case 2: t1[i][j] = x; break;
+              case 3: t1[i][j] = __fadd_rn(t1[i][j], x); t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]); break;
+              case 4: t1[i][j] = x; break;
+              case 5: t1[i][j] = __fadd_rn(t1[i][j], x); break;
+              case 6: t2[i][j] = x; break;
+              default:
+                t2[i][j] = __fadd_rn(t2[i][j], x);
+                t1[i][j] = __fadd_rn(t1[i][j], t2[i][j]);
+                t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]);
+            }
+          }
+      }
+      for (int q = G.qb[8]; q < G.qb[9]; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (rq * 4 + j >= m) break;
-      const int row = __ldg(rows + rq * 4 + j);
+        for (int j = 0; j < RR; ++j) {
+          const float b = __ldg(B + q * m4 + j);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        s.ZS[(pq * 4 + i) * a.ldz + row] = post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j];
+          for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], b));
+        }
+      }
+      const int32_t* rows = a.index + G.row;
+#pragma unroll
+      for (int j = 0; j < RR; ++j) {
+        if (r0 + j >= m) break;
+        const int row = __ldg(rows + r0 + j);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          s.ZS[(pq * 4 + i) * a.ldz + row] = post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j];
+      }
     }
   }
 }
@@ -448,7 +472,8 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
 }
 
 template <class T, int KID>
-__global__ void __launch_bounds__(NT, 2) evaluate_kernel(const Args<T> a) {
+__global__ void __launch_bounds__(NT, sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MIN_BLOCKS_F32)
+    evaluate_kernel(const Args<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);
   load_plan(a, s);

@@ -37,8 +37,13 @@ template <> struct M<double> {
 };
 
 template <> struct M<float> {
+#if RB_F32_POLY
+  static __device__ __forceinline__ float cos(float x) { return fast_cosf(x); }
+  static __device__ __forceinline__ float sin(float x) { return fast_sinf(x); }
+#else
   static __device__ __forceinline__ float cos(float x) { return (float)fast_cos((double)x); }
   static __device__ __forceinline__ float sin(float x) { return (float)fast_sin((double)x); }
+#endif
   static __device__ __forceinline__ float exp(float x) { return (float)::exp((double)x); }
   static __device__ __forceinline__ float log(float x) { return (float)::log((double)x); }
   static __device__ __forceinline__ float expm1(float x) { return (float)::expm1((double)x); }
@@ -75,11 +80,17 @@ template <class T> __device__ __forceinline__ T C(double v) { return static_cast
 //   > 128     : pw(first m) + pw(rest), m = n/2 rounded down to a multiple of 8
 // Lane k is accumulator r_k; the combine is the xor butterfly 1, 2, 4.
 // f is called once per element, by the lane that owns it.
+#ifndef RB_LEAF_UNROLL
+#define RB_LEAF_UNROLL 2
+#endif
+constexpr int kLeafUnroll = RB_LEAF_UNROLL;   // independent kernel terms in flight per lane
+
 template <class T, class F>
 __device__ __forceinline__ T pw8_leaf(int lo, int n, F& f, int l8) {
   T r = T(0);
   const int main_len = n < 8 ? 0 : n - (n & 7);
   if (main_len) {
+#pragma unroll kLeafUnroll
     for (int i = l8; i < main_len; i += 8) r = r + f(lo + i);
     r = r + __shfl_xor_sync(RB_FULL, r, 1, 8);
     r = r + __shfl_xor_sync(RB_FULL, r, 2, 8);
@@ -93,14 +104,55 @@ __device__ __forceinline__ T pw8_leaf(int lo, int n, F& f, int l8) {
   return r;
 }
 
+// n > 128: NumPy splits recursively, pw(a, n) = pw(a, m) + pw(a + m, n - m)
+// with m = n/2 rounded down to a multiple of 8.  Iterative post-order walk
+// (no device recursion: its stack frames overflowed once the leaf loop was
+// unrolled); every lane of the group walks the same tree.
 template <class T, class F>
-__device__ T pw8_tree(int lo, int n, F& f, int l8) {
-  if (n <= 128) return pw8_leaf<T>(lo, n, f, l8);
-  int m = n >> 1;
-  m -= m & 7;
-  const T a = pw8_tree<T>(lo, m, f, l8);
-  const T b = pw8_tree<T>(lo + m, n - m, f, l8);
-  return a + b;
+__device__ __noinline__ T pw8_tree(int lo, int n, F& f, int l8) {
+  constexpr int kDepth = 24;                 // n < 128 * 2^23
+  int s_lo[kDepth], s_n[kDepth], s_stage[kDepth];
+  T s_left[kDepth];
+  int sp = 0;
+  s_lo[0] = lo;
+  s_n[0] = n;
+  s_stage[0] = 0;
+  T val = T(0);
+  bool have = false;                         // `val` holds a finished subtree
+  while (sp >= 0) {
+    const int cl = s_lo[sp], cn = s_n[sp];
+    if (have) {                              // a child finished
+      if (s_stage[sp] == 1) {                // left child: descend right
+        s_left[sp] = val;
+        s_stage[sp] = 2;
+        int m = cn >> 1;
+        m -= m & 7;
+        ++sp;
+        s_lo[sp] = cl + m;
+        s_n[sp] = cn - m;
+        s_stage[sp] = 0;
+        have = false;
+      } else {                               // right child: combine, pop
+        val = s_left[sp] + val;
+        --sp;
+      }
+      continue;
+    }
+    if (cn <= 128) {                         // leaf
+      val = pw8_leaf<T>(cl, cn, f, l8);
+      have = true;
+      --sp;
+      continue;
+    }
+    int m = cn >> 1;                         // descend left
+    m -= m & 7;
+    s_stage[sp] = 1;
+    ++sp;
+    s_lo[sp] = cl;
+    s_n[sp] = m;
+    s_stage[sp] = 0;
+  }
+  return val;
 }
 
 template <class T, class F>
