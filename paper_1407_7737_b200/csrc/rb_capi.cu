@@ -174,8 +174,7 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   RB_CUDA(cudaStreamSynchronize(stream));
   const int flag = e->h_flags[slot];
   if (prev != e->device) cudaSetDevice(prev);
-  if (flag & 1) return fail(RB_E_NON_FINITE_INPUT, "batch contains NaN or infinity");
-  if (flag & 2) return fail(RB_E_NON_FINITE_INPUT, "kernel input contains NaN or infinity");
+  if (flag) return fail(RB_E_NON_FINITE_INPUT, "batch contains NaN or infinity (kernel input not finite)");
   return RB_OK;
 }
 
@@ -241,7 +240,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       const rb_segment& sg = pk->segments[si];
       int q4 = 0;
       for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
-        max_q += pk->groups[g].m;
+        max_q += rb::round8(pk->groups[g].m);
         q4 += (pk->groups[g].m + 3) & ~3;
       }
       ldv = std::max(ldv, q4);

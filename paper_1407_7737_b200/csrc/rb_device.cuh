@@ -2,19 +2,22 @@
 // instantiation units rb_kern_f64.cu / rb_kern_f32.cu.
 //
 // Persistent grid; one CTA (256 threads) walks tiles of TP = 32 points:
-//   load     X tile -> XS via one TMA bulk copy (cp.async.bulk + mbarrier)
+//   load     X tile -> XS via one TMA bulk copy (cp.async.bulk + mbarrier),
+//            double-buffered when shared memory allows (next tile in flight)
 //   rotate   z = R (scale*(x - o)[perm] + pre) + post per diagonal block
-//              fp64: warp strips of 16 points x 40 rows on the tensor pipe,
-//                    mma.sync.m16n8k4.f64 (DMMA); the shift/scale is applied
-//                    while building the A fragments straight from XS, the B
-//                    fragments come pre-swizzled from the pack (one 256-byte
-//                    coalesced load per fragment)
+//              fp64: mma.sync.m16n8k4.f64 (DMMA) on the tensor pipe.  The
+//                    segment's (m-tile, n-tile) units are split into 8 equal
+//                    contiguous ranges, one per warp; A fragments are built in
+//                    registers from XS (shift/scale fused), B fragments come
+//                    pre-swizzled from the pack (one 256-byte load each)
 //              fp32: SIMT FMUL+FADD in NumPy's pairwise order (bit-exact z),
 //                    4 points x 4 rows per thread from a q-ordered V tile
+//            the epilogue scatters z into ZS and checks it is finite (the
+//            reference's NonFiniteInput, engine.py:202-203, kernels.py:45-49)
 //   kernel   8 lanes per point, NumPy-order reductions (rb_kernels.cuh)
 //   blend    composition weights / member sum (composition.py:114-166)
-// The function's descriptors and per-column gather tables are copied into
-// shared memory once per CTA ("plan").
+// The function's descriptors and per-column gather tables live in shared
+// memory for the CTA's lifetime ("plan").
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,13 +25,6 @@
 #include "../../include/robench_b200.h"
 #include "rb_kernels.cuh"
 
-namespace rb {
-
-constexpr int TP = 32;          // points per tile
-constexpr int NT = 256;         // threads per CTA = 8 lanes x TP
-constexpr int MAX_MEMBERS = 5;
-constexpr int MAX_SEGMENTS = 16;
-constexpr int MAX_GROUPS = 16;
 #ifndef RB_NTC
 #define RB_NTC 2
 #endif
@@ -41,7 +37,16 @@ constexpr int MAX_GROUPS = 16;
 #ifndef RB_F32_ROWS
 #define RB_F32_ROWS 4             // rows per pass of the float32 rotate tile (4 or 2)
 #endif
-constexpr int NTC = RB_NTC;     // DMMA n-tiles (8 rows) per warp strip
+
+namespace rb {
+
+constexpr int TP = 32;          // points per tile
+constexpr int NT = 256;         // threads per CTA = 8 lanes x TP
+constexpr int NWARPS = NT / 32;
+constexpr int MAX_MEMBERS = 5;
+constexpr int MAX_SEGMENTS = 16;
+constexpr int MAX_GROUPS = 16;
+constexpr int NTC = RB_NTC;     // DMMA n-tiles (8 rows) accumulated per pass
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
 template <class T>
@@ -57,10 +62,10 @@ struct Args {
   const int32_t* index;
   const T* values;
   int fn;
-  int* flag;        // bit 0: non-finite x, bit 1: non-finite kernel input
+  int* flag;        // set to 2 when a kernel input is not finite
   int ldz;          // ZS row stride (elements)
   int ldv;          // fp32 V tile rows (sum of 4-padded group sizes)
-  int max_q;        // capacity of the plan's gather tables
+  int max_q;        // capacity of the plan's per-column tables
   int tma;          // x is 16-byte aligned: bulk-copy full tiles
   int nbuf;         // 2: prefetch the next tile while computing this one
 };
@@ -71,16 +76,21 @@ struct PlanHead {
   rb_member mem[MAX_MEMBERS];
   rb_segment seg[MAX_SEGMENTS];
   rb_group grp[MAX_GROUPS];
-  int gq0[MAX_GROUPS];            // group g's slice of the gather tables
+  int gq0[MAX_GROUPS];            // group g's slice of the per-column tables (8-aligned)
   unsigned long long mbar[2];     // TMA completion barriers, one per X buffer
+  uint32_t live;                  // points of the tile whose kernel inputs are checked
 };
 
-// dynamic shared memory: [PlanHead][qsrc int[max_q]][qo T[max_q]][XB0 (XB1)][V][ZS]
+__host__ __device__ inline int round8(int v) { return (v + 7) & ~7; }
+
+// dynamic shared memory:
+//   [PlanHead][qsrc int[max_q]][prow int[max_q]][qo T[max_q]][XB0 (XB1)][V][ZS]
 template <class T>
 struct Smem {
   PlanHead* P;
   int* qsrc;      // x column feeding the group's q-th column (split perm applied)
-  T* qo;          // the optimum at that column
+  int* prow;      // z position of the group's r-th block row
+  T* qo;          // the optimum at the q-th column
   T* XS;          // [TP][dim], the current tile (one of XB)
   T* XB[2];       // X tile buffers (XB[1] == XB[0] without prefetch)
   T* VS;          // fp32 only: [ldv][TP]
@@ -92,7 +102,7 @@ __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(
 template <class T>
 __host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q, int nbuf) {
   size_t b = align16(sizeof(PlanHead));
-  b += align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
+  b += 2 * align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
   b += nbuf * align16(sizeof(T) * TP * dim);
   if (sizeof(T) == 4) b += align16(sizeof(T) * TP * ldv);
   b += align16(sizeof(T) * TP * ldz);
@@ -106,6 +116,8 @@ __device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
   s.P = reinterpret_cast<PlanHead*>(base);
   off += align16(sizeof(PlanHead));
   s.qsrc = reinterpret_cast<int*>(base + off);
+  off += align16(sizeof(int) * a.max_q);
+  s.prow = reinterpret_cast<int*>(base + off);
   off += align16(sizeof(int) * a.max_q);
   s.qo = reinterpret_cast<T*>(base + off);
   off += align16(sizeof(T) * a.max_q);
@@ -130,7 +142,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 // ------------------------------------------------------------------ plan
 // Copy the function's descriptors (contiguous in the pack) into shared
-// memory and build the per-group gather tables.
+// memory and build the per-column gather tables (padded to 8 columns with
+// column 0 and optimum 0: finite values times zero B entries) and the
+// per-row scatter table.
 template <class T>
 __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
   PlanHead& P = *s.P;
@@ -158,11 +172,10 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
     int q = 0;
     for (int g = 0; g < P.n_grp; ++g) {
       P.gq0[g] = q;
-      q += P.grp[g].m;
+      q += round8(P.grp[g].m);
     }
   }
   __syncthreads();
-  // gather tables: walk members -> segments -> groups
   for (int mi = 0; mi < P.fn.n_members; ++mi) {
     const rb_member& mem = P.mem[mi];
     const T* o = a.values + mem.shift;
@@ -172,11 +185,19 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
         const int g = seg.group0 - P.grp_base + gi;
         const rb_group& G = P.grp[g];
         const int32_t* cols = a.index + G.col;
-        for (int q = threadIdx.x; q < G.m; q += NT) {
-          const int pos = cols[q];
-          const int src = mem.perm >= 0 ? a.index[mem.perm + seg.src + pos] : pos;
+        const int32_t* rows = a.index + G.row;
+        for (int q = threadIdx.x; q < round8(G.m); q += NT) {
+          int src = 0, row = 0;
+          T ov = T(0);
+          if (q < G.m) {
+            const int pos = cols[q];
+            src = mem.perm >= 0 ? a.index[mem.perm + seg.src + pos] : pos;
+            ov = o[src];
+            row = rows[q];
+          }
           s.qsrc[P.gq0[g] + q] = src;
-          s.qo[P.gq0[g] + q] = o[src];
+          s.qo[P.gq0[g] + q] = ov;
+          s.prow[P.gq0[g] + q] = row;
         }
       }
     }
@@ -225,6 +246,14 @@ __device__ __forceinline__ void wait_tile(unsigned long long* mbar, uint32_t pha
   }
 }
 
+// z value into ZS; flags a non-finite value of a live point (kernels.py:45-49)
+template <class T>
+__device__ __forceinline__ void put_z(const Args<T>& a, const Smem<T>& s, int p, int pos, T v,
+                                      bool& bad) {
+  s.ZS[p * a.ldz + pos] = v;
+  bad |= !M<T>::finite(v) && ((s.P->live >> p) & 1u);
+}
+
 // ------------------------------------------------------------ rotate fp64
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b) {
   asm volatile(
@@ -235,34 +264,33 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
 }
 
 // z[p][row] = post + sum_q (scale*(x[p][src_q] - o_q) + pre) * B[q][r]
-// Warp task = (group, 16-point m-tile, chunk of NTC n-tiles).  A fragments
-// (a_i = (point gid + 8i, column tig)) are formed in registers from XS; B
-// fragments are pre-swizzled in the pack (rb_group::frag).
-__device__ inline void rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
+// Units = (group, 16-point m-tile, 8-row n-tile), ordered group-major; warp
+// w owns units [w*U/8, (w+1)*U/8) and walks them in runs of <= NTC n-tiles
+// that share (group, m-tile), so one A fragment per k-step feeds the run.
+// Fragment layouts (PTX m16n8k4 .f64): a_i = (gid + 8i, tig), b = (tig, gid),
+// c_i = (gid + 8*(i>>1), 2*tig + (i&1)).
+__device__ inline bool rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
   const PlanHead& P = *s.P;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const double scale = seg.scale, pre = seg.pre, post = seg.post;
   const int g0 = seg.group0 - P.grp_base;
   int total = 0;
-  for (int g = 0; g < seg.n_groups; ++g) {
-    const int ntn = (P.grp[g0 + g].m + 7) >> 3;
-    total += (TP / 16) * ((ntn + NTC - 1) / NTC);
-  }
-  for (int t = warp; t < total; t += NT / 32) {
-    int g = g0, rem = t;
+  for (int g = 0; g < seg.n_groups; ++g) total += (TP / 16) * ((P.grp[g0 + g].m + 7) >> 3);
+  const int end = (warp + 1) * total / NWARPS;
+  bool bad = false;
+  for (int u = warp * total / NWARPS; u < end;) {
+    int g = g0, rem = u;
     for (;;) {
-      const int ntn = (P.grp[g].m + 7) >> 3;
-      const int cnt = (TP / 16) * ((ntn + NTC - 1) / NTC);
+      const int cnt = (TP / 16) * ((P.grp[g].m + 7) >> 3);
       if (rem < cnt) break;
       rem -= cnt;
       ++g;
     }
     const rb_group& G = P.grp[g];
     const int m = G.m, ntn = (m + 7) >> 3, nks = (m + 3) >> 2;
-    const int nch = (ntn + NTC - 1) / NTC;
-    const int mt = rem / nch, ch = rem - mt * nch;
-    const int nt0 = ch * NTC, ncnt = min(NTC, ntn - nt0);
+    const int mt = rem / ntn, nt0 = rem - mt * ntn;
+    const int run = min(min(NTC, ntn - nt0), end - u);
     const double* F = a.values + G.frag + (size_t)nt0 * nks * 32 + lane;
     const int* qs = s.qsrc + P.gq0[g];
     const double* qo = s.qo + P.gq0[g];
@@ -275,59 +303,49 @@ __device__ inline void rotate(const Args<double>& a, const Smem<double>& s, cons
       for (int i = 0; i < 4; ++i) acc[c][i] = 0.0;
 #pragma unroll 2
     for (int ks = 0; ks < nks; ++ks) {
-      const int q = ks * 4 + tig;
-      double a0 = 0.0, a1 = 0.0;
-      if (q < m) {
-        const int col = qs[q];
-        const double o = qo[q];
-        a0 = scale * (X0[col] - o);
-        a1 = scale * (X1[col] - o);
-        if (pre != 0.0) {
-          a0 = a0 + pre;
-          a1 = a1 + pre;
-        }
-      }
+      const int q = ks * 4 + tig;               // padded columns read x[.][0] * B = 0
+      const int col = qs[q];
+      const double o = qo[q];
+      const double a0 = scale * (X0[col] - o) + pre;
+      const double a1 = scale * (X1[col] - o) + pre;
 #pragma unroll
       for (int c = 0; c < NTC; ++c)
-        if (c < ncnt) dmma_16x8x4(acc[c], a0, a1, __ldg(F + (c * nks + ks) * 32));
+        if (c < run) dmma_16x8x4(acc[c], a0, a1, __ldg(F + (c * nks + ks) * 32));
     }
-    const int32_t* rows = a.index + G.row;
+    const int* prow = s.prow + P.gq0[g];
 #pragma unroll
     for (int c = 0; c < NTC; ++c) {
-      if (c >= ncnt) break;
+      if (c >= run) break;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int rr = (nt0 + c) * 8 + 2 * tig + (i & 1);
-        const int pp = mt * 16 + gid + ((i >> 1) << 3);
-        if (rr < m) s.ZS[pp * a.ldz + __ldg(rows + rr)] = post != 0.0 ? acc[c][i] + post : acc[c][i];
+        if (rr < m) put_z(a, s, mt * 16 + gid + ((i >> 1) << 3), prow[rr], acc[c][i] + post, bad);
       }
     }
+    u += run;
   }
+  return bad;
 }
 
 // ------------------------------------------------------------ rotate fp32
 // Exact NumPy order (transforms.py:42-48): rounded products, per-slot
 // accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
 // ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
-__device__ inline void rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
+__device__ inline bool rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
   const PlanHead& P = *s.P;
   const int g0 = seg.group0 - P.grp_base;
   const float scale = (float)seg.scale, pre = (float)seg.pre, post = (float)seg.post;
-  // gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre
+  // gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre   (engine.py:97-100)
   {
     int vq = 0;
     for (int g = 0; g < seg.n_groups; ++g) {
-      const rb_group& G = P.grp[g0 + g];
-      const int kp = round4(G.m);
+      const int kp = round4(P.grp[g0 + g].m);
       const int* qs = s.qsrc + P.gq0[g0 + g];
       const float* qo = s.qo + P.gq0[g0 + g];
       for (int e = threadIdx.x; e < TP * kp; e += NT) {
         const int q = e / TP, p = e - q * TP;
-        float v = 0.0f;
-        if (q < G.m) {
-          v = scale * (s.XS[p * a.dim + qs[q]] - qo[q]);
-          if (pre != 0.0f) v = v + pre;
-        }
+        float v = scale * (s.XS[p * a.dim + qs[q]] - qo[q]);
+        if (pre != 0.0f) v = v + pre;
         s.VS[(vq + q) * TP + p] = v;
       }
       vq += kp;
@@ -336,6 +354,7 @@ __device__ inline void rotate(const Args<float>& a, const Smem<float>& s, const 
   __syncthreads();
   int total = 0;
   for (int g = 0; g < seg.n_groups; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
+  bool bad = false;
   for (int t = threadIdx.x; t < total; t += NT) {
     int g = g0, rem = t, vq = 0;
     for (;;) {
@@ -348,6 +367,7 @@ __device__ inline void rotate(const Args<float>& a, const Smem<float>& s, const 
     const rb_group& G = P.grp[g];
     const int pq = rem & 7, rq = rem >> 3;
     const int m = G.m, m4 = round4(m);
+    const int* prow = s.prow + P.gq0[g];
     constexpr int RR = RB_F32_ROWS;
 #pragma unroll 1
     for (int pass = 0; pass < 4 / RR; ++pass) {
@@ -407,64 +427,59 @@ __device__ inline void rotate(const Args<float>& a, const Smem<float>& s, const 
           for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], b));
         }
       }
-      const int32_t* rows = a.index + G.row;
 #pragma unroll
       for (int j = 0; j < RR; ++j) {
         if (r0 + j >= m) break;
-        const int row = __ldg(rows + r0 + j);
+        const int row = prow[r0 + j];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          s.ZS[(pq * 4 + i) * a.ldz + row] = post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j];
+          put_z(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j], bad);
       }
     }
   }
+  return bad;
 }
 
 // ---------------------------------------------------------- one segment
+// z of one segment into ZS (all points of the tile), then barrier.
 template <class T>
 __device__ void stage_segment(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
                               const rb_segment& seg) {
-  if (seg.n_groups == 0) {                 // shift-only ids 10 and 15
+  bool bad;
+  if (seg.n_groups == 0) {                 // shift-only ids 10 and 15 (engine.py:96-104)
     const T* o = a.values + mem.shift;
     const int32_t* perm = mem.perm >= 0 ? a.index + mem.perm + seg.src : nullptr;
     const T scale = (T)seg.scale, pre = (T)seg.pre, post = (T)seg.post;
-    const int d = seg.d;
-    for (int e = threadIdx.x; e < TP * d; e += NT) {
-      const int p = e / d, j = e - p * d;
+    const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+    bad = false;
+    for (int j = l8; j < seg.d; j += 8) {
       const int src = perm ? perm[j] : j;
       T v = scale * (s.XS[p * a.dim + src] - o[src]);
       if (pre != T(0)) v = v + pre;
       if (post != T(0)) v = v + post;
-      s.ZS[p * a.ldz + j] = v;
+      put_z(a, s, p, j, v, bad);
     }
   } else {
-    rotate(a, s, seg);
+    bad = rotate(a, s, seg);
   }
+  if (bad) atomicOr(a.flag, 2);
   __syncthreads();
 }
 
+// Value of one member (basic function, hybrid, or composition member) for
+// the calling lane's point.
 template <class T, int KID>
-__device__ __forceinline__ T segment_value(const Smem<T>& s, const rb_segment& seg, const T* ctab,
-                                           int p, int l8, const Args<T>& a, bool live) {
-  const T* z = s.ZS + p * a.ldz;
-  bool bad = false;
-  for (int j = l8; j < seg.d; j += 8) bad |= !M<T>::finite(z[j]);   // kernels.py:45-49
-  if (bad && live) atomicOr(a.flag, 2);
-  const Pt<T> pt{z, seg.d, l8, ctab};
-  if constexpr (KID >= 0) return kernel_value_k<T, KID>(pt);
-  else return kernel_value<T>(seg.kernel, pt);
-}
-
-// Value of one member (basic function, hybrid, or composition member).
-template <class T, int KID>
-__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, bool live) {
+__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem) {
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
   T total = T(0);
   for (int si = 0; si < mem.n_segments; ++si) {
     const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
     stage_segment(a, s, mem, seg);
-    const T v = segment_value<T, KID>(s, seg, a.values + seg.ctab, p, l8, a, live);
+    const Pt<T> pt{s.ZS + p * a.ldz, seg.d, l8, a.values + seg.ctab};
+    T v;
+    if constexpr (KID >= 0) v = kernel_value_k<T, KID>(pt);
+    else v = kernel_value<T>(seg.kernel, pt);
     total = (si == 0) ? v : total + v;   // hybrid.py:105-115: 0 + K_0 + K_1 + ...
     __syncthreads();                      // ZS is rewritten by the next segment
   }
@@ -477,13 +492,13 @@ __global__ void __launch_bounds__(NT, sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MI
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);
   load_plan(a, s);
-  const PlanHead& P = *s.P;
+  PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
   uint32_t phase0 = 0u, phase1 = 0u;
   const int64_t first = blockIdx.x;
   if (a.nbuf == 2 && threadIdx.x == 0 && first < ntiles && tile_is_bulk(a, tile_rows(a, first)))
-    issue_tile(a, s.XB[0], &s.P->mbar[0], first, tile_rows(a, first));
+    issue_tile(a, s.XB[0], &P.mbar[0], first, tile_rows(a, first));
 
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
@@ -492,38 +507,36 @@ __global__ void __launch_bounds__(NT, sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MI
     st.XS = b ? s.XB[1] : s.XB[0];
     const int64_t row0 = tile * TP;
     const int nv = tile_rows(a, tile);
+    const uint32_t valid_mask = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
     const int64_t next = tile + gridDim.x;
     if (threadIdx.x == 0) {
       if (a.nbuf == 2 && next < ntiles && tile_is_bulk(a, tile_rows(a, next)))
-        issue_tile(a, b ? s.XB[0] : s.XB[1], b ? &s.P->mbar[0] : &s.P->mbar[1], next,
+        issue_tile(a, b ? s.XB[0] : s.XB[1], b ? &P.mbar[0] : &P.mbar[1], next,
                    tile_rows(a, next));
-      if (a.nbuf == 1 && tile_is_bulk(a, nv)) issue_tile(a, st.XS, &s.P->mbar[0], tile, nv);
+      if (a.nbuf == 1 && tile_is_bulk(a, nv)) issue_tile(a, st.XS, &P.mbar[0], tile, nv);
+      P.live = valid_mask;
     }
     if (tile_is_bulk(a, nv)) {
       if (b) {
-        wait_tile(&s.P->mbar[1], phase1);
+        wait_tile(&P.mbar[1], phase1);
         phase1 ^= 1u;
       } else {
-        wait_tile(&s.P->mbar[0], phase0);
+        wait_tile(&P.mbar[0], phase0);
         phase0 ^= 1u;
       }
     } else {
       const T* src = a.x + row0 * a.dim;
       for (int e = threadIdx.x; e < nv * a.dim; e += NT) st.XS[e] = src[e];
-      __syncthreads();
-    }
-    {                                                     // engine.py:202-203
-      bool bad = false;
-      for (int e = threadIdx.x; e < nv * a.dim; e += NT) bad |= !M<T>::finite(st.XS[e]);
-      if (bad) atomicOr(a.flag, 1);
     }
     __syncthreads();
+    // A non-finite x reaches some z of every evaluated member, so the z
+    // checks cover the batch check of engine.py:202-203 as well.
     const bool valid = p < nv;
     T result;
     if constexpr (KID >= 0) {
-      result = member_value<T, KID>(a, st, P.mem[0], valid);
+      result = member_value<T, KID>(a, st, P.mem[0]);
     } else if (P.fn.category != RB_COMPOSITION) {
-      result = member_value<T, GENERIC>(a, st, P.mem[0], valid);
+      result = member_value<T, GENERIC>(a, st, P.mem[0]);
     } else {
       // composition.py:114-141: weights from the squared distances
       const int nm = P.fn.n_members;
@@ -562,7 +575,7 @@ __global__ void __launch_bounds__(NT, sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MI
         for (int k = 0; k < MAX_MEMBERS; ++k)
           if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;
       }
-      // composition.py:157-166: zero weights are skipped
+      // composition.py:157-166: zero weights are skipped (and not checked)
       T total = T(0);
 #pragma unroll 1
       for (int k = 0; k < nm; ++k) {
@@ -571,9 +584,13 @@ __global__ void __launch_bounds__(NT, sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MI
         for (int kk = 0; kk < MAX_MEMBERS; ++kk)
           if (kk == k) omk = om[kk];
         const bool use = valid && omk != T(0);
+        __syncthreads();                                   // previous member done with P.live
+        if (threadIdx.x == 0) P.live = 0u;
+        __syncthreads();
+        if (l8 == 0 && use) atomicOr(&P.live, 1u << p);
         if (!__syncthreads_or(use)) continue;
         const rb_member& mem = P.mem[k];
-        const T g = member_value<T, GENERIC>(a, st, mem, use);
+        const T g = member_value<T, GENERIC>(a, st, mem);
         if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
       }
       result = total;
