@@ -15,6 +15,8 @@
 namespace rb {
 extern const void* const kernels_f64[N_VARIANTS];
 extern const void* const kernels_f32[N_VARIANTS];
+cudaError_t set_weier_f64(const double* a_then_c);
+cudaError_t set_weier_f32(const float* a_then_c);
 
 __global__ void np_powf_kernel(const float* x, const float* y, float* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -286,6 +288,31 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
   return RB_OK;
 }
 
+// Weierstrass series constants (a_k, c_k; pack.py kernel_constants) into
+// the kernels' __constant__ tables.  They depend on the dtype only, so every
+// Weierstrass segment of the pack must carry the same 42 values.
+rb_status upload_series_constants(const rb_pack* pk) {
+  int found = -1;
+  for (int i = 0; i < pk->n_segments; ++i) {
+    const rb_segment& s = pk->segments[i];
+    if (s.kernel != rb::K_WEIERSTRASS) continue;
+    if (s.ctab < 0 || (int64_t)s.ctab + 43 > pk->n_values)
+      return fail(RB_E_INVALID_ARGUMENT, "segment " + std::to_string(i) + ": constant table out of range");
+    if (found < 0) {
+      found = s.ctab;
+      continue;
+    }
+    for (int k = 0; k < 42; ++k)
+      if (pk->values_f64[s.ctab + k] != pk->values_f64[found + k] ||
+          pk->values_f32[s.ctab + k] != pk->values_f32[found + k])
+        return fail(RB_E_INVALID_ARGUMENT, "Weierstrass constant tables differ between segments");
+  }
+  if (found < 0) return RB_OK;
+  RB_CUDA(rb::set_weier_f64(pk->values_f64 + found));
+  RB_CUDA(rb::set_weier_f32(pk->values_f32 + found));
+  return RB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -336,6 +363,7 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   e->max_concurrency = max_concurrency;
   e->fns.assign(pk->functions, pk->functions + pk->n_functions);
   rb_status s = plan_launches(e, pk, device);
+  if (s == RB_OK) s = upload_series_constants(pk);
   if (s == RB_OK) s = upload(&e->d_fns, pk->functions, pk->n_functions);
   if (s == RB_OK) s = upload(&e->d_members, pk->members, pk->n_members);
   if (s == RB_OK) s = upload(&e->d_segments, pk->segments, pk->n_segments);

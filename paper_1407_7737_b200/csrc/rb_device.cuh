@@ -486,8 +486,14 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
   return total;
 }
 
+// Resident CTAs per SM the register budget is sized for.
 template <class T, int KID>
-__global__ void __launch_bounds__(NT, sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MIN_BLOCKS_F32)
+constexpr int min_blocks() {
+  return sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MIN_BLOCKS_F32;
+}
+
+template <class T, int KID>
+__global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     evaluate_kernel(const Args<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);

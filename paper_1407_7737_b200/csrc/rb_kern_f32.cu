@@ -19,4 +19,10 @@ extern const void* const kernels_f32[N_VARIANTS] = {
     (const void*)evaluate_kernel<float, 20>, (const void*)evaluate_kernel<float, GENERIC>,
 };
 
+// Series constants of this unit's Weierstrass kernels (rb_kernels.cuh);
+// each translation unit owns its __constant__ copy.
+cudaError_t set_weier_f32(const float* a_then_c) {
+  return cudaMemcpyToSymbol(kWei32, a_then_c, sizeof(WeierTab<float>));
+}
+
 }  // namespace rb

@@ -19,4 +19,10 @@ extern const void* const kernels_f64[N_VARIANTS] = {
     (const void*)evaluate_kernel<double, 20>, (const void*)evaluate_kernel<double, GENERIC>,
 };
 
+// Series constants of this unit's Weierstrass kernels (rb_kernels.cuh);
+// each translation unit owns its __constant__ copy.
+cudaError_t set_weier_f64(const double* a_then_c) {
+  return cudaMemcpyToSymbol(kWei64, a_then_c, sizeof(WeierTab<double>));
+}
+
 }  // namespace rb
