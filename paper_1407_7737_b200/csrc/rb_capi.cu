@@ -74,6 +74,15 @@ int prefetch_mode() {
   return v ? std::atoi(v) : -1;
 }
 
+// RB_L2PF=0 disables the L2 prefetch of upcoming X tiles (default on).
+int l2_prefetch() {
+  static const int v = [] {
+    const char* e = std::getenv("RB_L2PF");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 }  // namespace
 
 struct rb_engine {
@@ -167,6 +176,7 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   a.max_q = L.max_q;
   a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
   a.nbuf = L.nbuf;
+  a.l2pf = l2_prefetch();
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
   void* args[] = {&a};
@@ -237,17 +247,20 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
     const int g1 = pk->segments[s1 - 1].group0 + pk->segments[s1 - 1].n_groups;
     if (fn.n_members > rb::MAX_MEMBERS || s1 - s0 > rb::MAX_SEGMENTS || g1 - g0 > rb::MAX_GROUPS)
       return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the plan limits");
-    int max_q = 0, ldv = 4;
+    int max_q = 0, ldv = 4, units = 0;
     for (int si = s0; si < s1; ++si) {
       const rb_segment& sg = pk->segments[si];
       int q4 = 0;
       for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
         max_q += rb::round8(pk->groups[g].m);
         q4 += (pk->groups[g].m + 3) & ~3;
+        units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
       }
       ldv = std::max(ldv, q4);
       if (sg.n_groups && sg.d > 128) e->exact_ok[fi] = 0;
     }
+    if (units > rb::MAX_UNITS)
+      return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the DMMA unit table");
     if (fn.category == RB_BASIC && fn.n_members == 1 && first.n_segments == 1)
       variant[fi] = pk->segments[s0].kernel;
     for (int pi = 0; pi < 2; ++pi) {
@@ -256,7 +269,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       L.max_q = std::max(max_q, 1);
       L.ldv = ldv;
       for (int nb = 1; nb <= 2; ++nb)
-        L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, ldv, e->ldz[0], L.max_q, nb)
+        L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, L.ldv, e->ldz[0], L.max_q, nb)
                                   : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q, nb);
       if ((int)L.smem_nbuf[1] > optin)
         return fail(RB_E_UNSUPPORTED, "dimension too large for the shared-memory tile");
@@ -281,6 +294,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       if (occ[1] < 1) return fail(RB_E_UNSUPPORTED, "kernel does not fit on an SM");
       const int mode = prefetch_mode();
       L.nbuf = (mode == 1 && occ[2] >= 1) || (mode < 0 && occ[2] >= occ[1]) ? 2 : 1;
+      if (pi == 0) L.nbuf = 1;           // fp64 tiles have no second X buffer
       L.smem = L.smem_nbuf[L.nbuf];
       L.grid_cap = sms * occ[L.nbuf];
     }

@@ -40,12 +40,16 @@
 
 namespace rb {
 
-constexpr int TP = 32;          // points per tile
-constexpr int NT = 256;         // threads per CTA = 8 lanes x TP
+#ifndef RB_TP
+#define RB_TP 32
+#endif
+constexpr int TP = RB_TP;       // points per tile (16 or 32)
+constexpr int NT = 8 * TP;      // threads per CTA = 8 lanes x TP
 constexpr int NWARPS = NT / 32;
 constexpr int MAX_MEMBERS = 5;
 constexpr int MAX_SEGMENTS = 16;
 constexpr int MAX_GROUPS = 16;
+constexpr int MAX_UNITS = 512;  // fp64 DMMA units (m-tile x n-tile of a group) per function
 constexpr int NTC = RB_NTC;     // DMMA n-tiles (8 rows) accumulated per pass
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
@@ -68,6 +72,7 @@ struct Args {
   int max_q;        // capacity of the plan's per-column tables
   int tma;          // x is 16-byte aligned: bulk-copy full tiles
   int nbuf;         // 2: prefetch the next tile while computing this one
+  int l2pf;         // 1: also pull the tile after the next in-flight one into L2
 };
 
 struct PlanHead {
@@ -79,18 +84,25 @@ struct PlanHead {
   int gq0[MAX_GROUPS];            // group g's slice of the per-column tables (8-aligned)
   unsigned long long mbar[2];     // TMA completion barriers, one per X buffer
   uint32_t live;                  // points of the tile whose kernel inputs are checked
+  int n_jobs;                     // (member, segment) pairs per tile, in evaluation order
+  int8_t job_mem[MAX_SEGMENTS];
+  int8_t job_seg[MAX_SEGMENTS];   // index into seg[]
+  int unit_off[MAX_SEGMENTS + 1];  // fp64 rotate: segment si's units are unit[unit_off[si] ..)
+  uint32_t unit[MAX_UNITS];       // (group | m-tile << 8 | n-tile << 16), group-major per segment
 };
 
 __host__ __device__ inline int round8(int v) { return (v + 7) & ~7; }
 
 // dynamic shared memory:
-//   [PlanHead][qsrc int[max_q]][prow int[max_q]][qo T[max_q]][XB0 (XB1)][V][ZS]
+//   fp32: [PlanHead][qsrc int[max_q]][prow int[max_q]][qo T[max_q]][XB0 (XB1)][V][ZS]
+//   fp64: [PlanHead][qsrc int[max_q]][prow int[max_q]][qo T[max_q]][cz T[max_q]][XS][ZS]
 template <class T>
 struct Smem {
   PlanHead* P;
   int* qsrc;      // x column feeding the group's q-th column (split perm applied)
   int* prow;      // z position of the group's r-th block row
   T* qo;          // the optimum at the q-th column
+  T* cz;          // fp64: offset constant of the r-th block row (pack.py group())
   T* XS;          // [TP][dim], the current tile (one of XB)
   T* XB[2];       // X tile buffers (XB[1] == XB[0] without prefetch)
   T* VS;          // fp32 only: [ldv][TP]
@@ -99,10 +111,13 @@ struct Smem {
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
+__host__ __device__ inline int imax(int a, int b) { return a > b ? a : b; }
+
 template <class T>
 __host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q, int nbuf) {
   size_t b = align16(sizeof(PlanHead));
   b += 2 * align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
+  if (sizeof(T) == 8) b += align16(sizeof(T) * max_q);
   b += nbuf * align16(sizeof(T) * TP * dim);
   if (sizeof(T) == 4) b += align16(sizeof(T) * TP * ldv);
   b += align16(sizeof(T) * TP * ldz);
@@ -121,6 +136,11 @@ __device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
   off += align16(sizeof(int) * a.max_q);
   s.qo = reinterpret_cast<T*>(base + off);
   off += align16(sizeof(T) * a.max_q);
+  s.cz = s.qo;
+  if (sizeof(T) == 8) {
+    s.cz = reinterpret_cast<T*>(base + off);
+    off += align16(sizeof(T) * a.max_q);
+  }
   s.XB[0] = reinterpret_cast<T*>(base + off);
   off += align16(sizeof(T) * TP * a.dim);
   s.XB[1] = s.XB[0];
@@ -159,14 +179,24 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
     const rb_segment sl = a.segments[last.segment0 + last.n_segments - 1];
     P.grp_base = s0.group0;
     P.n_grp = sl.group0 + sl.n_groups - s0.group0;
+    int nj = 0;
+    for (int mi = 0; mi < fn.n_members; ++mi) {
+      const rb_member mm = a.members[fn.member0 + mi];
+      for (int si = 0; si < mm.n_segments && nj < MAX_SEGMENTS; ++si, ++nj) {
+        P.job_mem[nj] = (int8_t)mi;
+        P.job_seg[nj] = (int8_t)(mm.segment0 - first.segment0 + si);
+      }
+    }
+    P.n_jobs = nj;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < P.fn.n_members; i += NT) P.mem[i] = a.members[P.fn.member0 + i];
-  for (int i = threadIdx.x; i < P.n_seg; i += NT) P.seg[i] = a.segments[P.seg_base + i];
-  for (int i = threadIdx.x; i < P.n_grp; i += NT) P.grp[i] = a.groups[P.grp_base + i];
+  const int nth = blockDim.x;
+  for (int i = threadIdx.x; i < P.fn.n_members; i += nth) P.mem[i] = a.members[P.fn.member0 + i];
+  for (int i = threadIdx.x; i < P.n_seg; i += nth) P.seg[i] = a.segments[P.seg_base + i];
+  for (int i = threadIdx.x; i < P.n_grp; i += nth) P.grp[i] = a.groups[P.grp_base + i];
   __syncthreads();
   if (threadIdx.x == 0) {
     int q = 0;
@@ -174,6 +204,16 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
       P.gq0[g] = q;
       q += round8(P.grp[g].m);
     }
+    int nu = 0;                              // fp64 DMMA units, group-major per segment
+    for (int si = 0; si < P.n_seg; ++si) {
+      P.unit_off[si] = nu;
+      const int g0 = P.seg[si].group0 - P.grp_base;
+      for (int g = g0; g < g0 + P.seg[si].n_groups; ++g)
+        for (int mt = 0; mt < TP / 16; ++mt)
+          for (int nt = 0; nt < (P.grp[g].m + 7) >> 3 && nu < MAX_UNITS; ++nt)
+            P.unit[nu++] = (uint32_t)g | ((uint32_t)mt << 8) | ((uint32_t)nt << 16);
+    }
+    P.unit_off[P.n_seg] = nu;
   }
   __syncthreads();
   for (int mi = 0; mi < P.fn.n_members; ++mi) {
@@ -186,18 +226,20 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
         const rb_group& G = P.grp[g];
         const int32_t* cols = a.index + G.col;
         const int32_t* rows = a.index + G.row;
-        for (int q = threadIdx.x; q < round8(G.m); q += NT) {
+        for (int q = threadIdx.x; q < round8(G.m); q += nth) {
           int src = 0, row = 0;
-          T ov = T(0);
+          T ov = T(0), cv = T(0);
           if (q < G.m) {
             const int pos = cols[q];
             src = mem.perm >= 0 ? a.index[mem.perm + seg.src + pos] : pos;
             ov = o[src];
             row = rows[q];
+            if (sizeof(T) == 8) cv = a.values[G.cz + q];     // indexed by block row q
           }
           s.qsrc[P.gq0[g] + q] = src;
           s.qo[P.gq0[g] + q] = ov;
           s.prow[P.gq0[g] + q] = row;
+          if (sizeof(T) == 8) s.cz[P.gq0[g] + q] = cv;
         }
       }
     }
@@ -234,6 +276,18 @@ __device__ __forceinline__ void issue_tile(const Args<T>& a, T* dst, unsigned lo
       : "memory");
 }
 
+// thread 0 only: warm L2 with a future tile (no shared memory needed), so
+// its TMA copy is served from L2 instead of HBM
+template <class T>
+__device__ __forceinline__ void prefetch_tile_l2(const Args<T>& a, int64_t tile) {
+  const int64_t ntiles = (a.n + TP - 1) / TP;
+  if (tile >= ntiles) return;
+  const uint32_t bytes = (uint32_t)(sizeof(T) * (size_t)tile_rows(a, tile) * a.dim) & ~15u;
+  if (!bytes || !a.tma) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + tile * TP * a.dim), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void wait_tile(unsigned long long* mbar, uint32_t phase) {
   const uint32_t bar = smem_u32(mbar);
   uint32_t done = 0;
@@ -246,12 +300,21 @@ __device__ __forceinline__ void wait_tile(unsigned long long* mbar, uint32_t pha
   }
 }
 
-// z value into ZS; flags a non-finite value of a live point (kernels.py:45-49)
+// NaN or infinity, by the exponent bits (integer pipe, not the FP64 pipe)
+__device__ __forceinline__ bool not_finite(double v) {
+  return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+}
+__device__ __forceinline__ bool not_finite(float v) {
+  return (__float_as_int(v) & 0x7f800000) == 0x7f800000;
+}
+
+// z value into ZS; records point p in `nf` when the value is not finite
+// (kernels.py:45-49).  stage_segment masks nf with the live points.
 template <class T>
 __device__ __forceinline__ void put_z(const Args<T>& a, const Smem<T>& s, int p, int pos, T v,
-                                      bool& bad) {
+                                      uint32_t& nf) {
   s.ZS[p * a.ldz + pos] = v;
-  bad |= !M<T>::finite(v) && ((s.P->live >> p) & 1u);
+  if (not_finite(v)) nf |= 1u << p;
 }
 
 // ------------------------------------------------------------ rotate fp64
@@ -263,37 +326,38 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b));
 }
 
-// z[p][row] = post + sum_q (scale*(x[p][src_q] - o_q) + pre) * B[q][r]
-// Units = (group, 16-point m-tile, 8-row n-tile), ordered group-major; warp
-// w owns units [w*U/8, (w+1)*U/8) and walks them in runs of <= NTC n-tiles
-// that share (group, m-tile), so one A fragment per k-step feeds the run.
-// Fragment layouts (PTX m16n8k4 .f64): a_i = (gid + 8i, tig), b = (tig, gid),
-// c_i = (gid + 8*(i>>1), 2*tig + (i&1)).
-__device__ inline bool rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
+// z[p][row_r] = sum_q (scale B)[q][r] (x[p][src_q] - o_q) - cz[r]
+//             = R (scale (x - o) + pre) + post   (engine.py:97-103, hybrid.py:103-114)
+// with the scale folded into the pack's B fragments and pre / post into one
+// constant per block row (pack.py group()), so an A element is one
+// subtraction -- exactly zero at the optimum, where z is then exactly post
+// as in the reference (HappyCat's |r2 - d|^0.25 would amplify any residue).
+// Summation order differs from NumPy's (float64 parity is to tolerance,
+// DESIGN.md section 3).
+// Units = (group, 16-point m-tile, 8-row n-tile), group-major (P.unit);
+// warp w owns units [w*U/NW, (w+1)*U/NW) and walks them in runs of <= NTC
+// n-tiles sharing (group, m-tile), so one A fragment per k-step feeds the
+// run.  Fragment layouts (PTX m16n8k4 .f64): a_i = (gid + 8i, tig),
+// b = (tig, gid), c_i = (gid + 8*(i>>1), 2*tig + (i&1)).
+template <int NW>
+__device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int si,
+                                      int warp) {
   const PlanHead& P = *s.P;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const double scale = seg.scale, pre = seg.pre, post = seg.post;
-  const int g0 = seg.group0 - P.grp_base;
-  int total = 0;
-  for (int g = 0; g < seg.n_groups; ++g) total += (TP / 16) * ((P.grp[g0 + g].m + 7) >> 3);
-  const int end = (warp + 1) * total / NWARPS;
-  bool bad = false;
-  for (int u = warp * total / NWARPS; u < end;) {
-    int g = g0, rem = u;
-    for (;;) {
-      const int cnt = (TP / 16) * ((P.grp[g].m + 7) >> 3);
-      if (rem < cnt) break;
-      rem -= cnt;
-      ++g;
-    }
+  const int u0 = P.unit_off[si];
+  const int total = P.unit_off[si + 1] - u0;
+  const int end = (warp + 1) * total / NW;
+  uint32_t nf = 0u;
+  for (int u = warp * total / NW; u < end;) {
+    const uint32_t ud = P.unit[u0 + u];
+    const int g = ud & 0xff, mt = (ud >> 8) & 0xff, nt0 = ud >> 16;
     const rb_group& G = P.grp[g];
     const int m = G.m, ntn = (m + 7) >> 3, nks = (m + 3) >> 2;
-    const int mt = rem / ntn, nt0 = rem - mt * ntn;
     const int run = min(min(NTC, ntn - nt0), end - u);
     const double* F = a.values + G.frag + (size_t)nt0 * nks * 32 + lane;
-    const int* qs = s.qsrc + P.gq0[g];
-    const double* qo = s.qo + P.gq0[g];
+    const int* qs = s.qsrc + P.gq0[g] + tig;    // padded columns read x[.][0] * B = 0
+    const double* qo = s.qo + P.gq0[g] + tig;
     const double* X0 = s.XS + (mt * 16 + gid) * a.dim;
     const double* X1 = X0 + 8 * a.dim;
     double acc[NTC][4];
@@ -301,37 +365,50 @@ __device__ inline bool rotate(const Args<double>& a, const Smem<double>& s, cons
     for (int c = 0; c < NTC; ++c)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[c][i] = 0.0;
-#pragma unroll 2
+#pragma unroll 3
     for (int ks = 0; ks < nks; ++ks) {
-      const int q = ks * 4 + tig;               // padded columns read x[.][0] * B = 0
-      const int col = qs[q];
-      const double o = qo[q];
-      const double a0 = scale * (X0[col] - o) + pre;
-      const double a1 = scale * (X1[col] - o) + pre;
+      const int col = qs[ks * 4];
+      const double o = qo[ks * 4];
+      const double a0 = X0[col] - o;
+      const double a1 = X1[col] - o;
 #pragma unroll
       for (int c = 0; c < NTC; ++c)
         if (c < run) dmma_16x8x4(acc[c], a0, a1, __ldg(F + (c * nks + ks) * 32));
     }
     const int* prow = s.prow + P.gq0[g];
+    const double* cz = s.cz + P.gq0[g];
+    const int p0 = mt * 16 + gid;
+    uint32_t e0 = 0u, e1 = 0u;                  // max exponent field per point
 #pragma unroll
     for (int c = 0; c < NTC; ++c) {
       if (c >= run) break;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int rr = (nt0 + c) * 8 + 2 * tig + (i & 1);
-        if (rr < m) put_z(a, s, mt * 16 + gid + ((i >> 1) << 3), prow[rr], acc[c][i] + post, bad);
+        if (rr < m) {
+          const double zv = acc[c][i] - cz[rr];
+          s.ZS[(p0 + ((i >> 1) << 3)) * a.ldz + prow[rr]] = zv;
+          const uint32_t e = (uint32_t)__double2hiint(zv) & 0x7ff00000u;
+          if (i < 2) e0 = max(e0, e); else e1 = max(e1, e);
+        }
       }
     }
+    if (e0 == 0x7ff00000u) nf |= 1u << p0;      // NaN or infinity (kernels.py:45-49)
+    if (e1 == 0x7ff00000u) nf |= 1u << (p0 + 8);
     u += run;
   }
-  return bad;
+  return nf;
+}
+
+__device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
+  return rotate_f64<NWARPS>(a, s, (int)(&seg - s.P->seg), threadIdx.x >> 5);
 }
 
 // ------------------------------------------------------------ rotate fp32
 // Exact NumPy order (transforms.py:42-48): rounded products, per-slot
 // accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
 // ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
-__device__ inline bool rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
+__device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
   const PlanHead& P = *s.P;
   const int g0 = seg.group0 - P.grp_base;
   const float scale = (float)seg.scale, pre = (float)seg.pre, post = (float)seg.post;
@@ -354,7 +431,7 @@ __device__ inline bool rotate(const Args<float>& a, const Smem<float>& s, const 
   __syncthreads();
   int total = 0;
   for (int g = 0; g < seg.n_groups; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
-  bool bad = false;
+  uint32_t nf = 0u;
   for (int t = threadIdx.x; t < total; t += NT) {
     int g = g0, rem = t, vq = 0;
     for (;;) {
@@ -365,7 +442,7 @@ __device__ inline bool rotate(const Args<float>& a, const Smem<float>& s, const 
       ++g;
     }
     const rb_group& G = P.grp[g];
-    const int pq = rem & 7, rq = rem >> 3;
+    const int pq = rem % (TP / 4), rq = rem / (TP / 4);
     const int m = G.m, m4 = round4(m);
     const int* prow = s.prow + P.gq0[g];
     constexpr int RR = RB_F32_ROWS;
@@ -433,55 +510,160 @@ __device__ inline bool rotate(const Args<float>& a, const Smem<float>& s, const 
         const int row = prow[r0 + j];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          put_z(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j], bad);
+          put_z(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j], nf);
       }
     }
   }
-  return bad;
+  return nf;
+}
+
+// ------------------------------------------------------------ tile state
+// The tile being evaluated, tracked identically by every thread of the CTA.
+struct TileCtx {
+  int64_t tile;
+  int nv;             // valid rows
+  uint32_t phase;     // parity of mbar[0] (fp64 loads / refetches)
+  bool x_ready;       // fp64: buffer A holds the X tile (not a segment's z)
+};
+
+// X tile into XS (buffer A for fp64); all threads; ends with a barrier.
+// The caller has passed a barrier since the last read of the buffer.
+template <class T>
+__device__ void fetch_x(const Args<T>& a, const Smem<T>& s, TileCtx& t) {
+  PlanHead& P = *s.P;
+  if (tile_is_bulk(a, t.nv)) {
+    if (threadIdx.x == 0) issue_tile(a, s.XS, &P.mbar[0], t.tile, t.nv);
+    wait_tile(&P.mbar[0], t.phase);
+    t.phase ^= 1u;
+  } else {
+    const T* src = a.x + t.tile * TP * a.dim;
+    for (int e = threadIdx.x; e < t.nv * a.dim; e += NT) s.XS[e] = src[e];
+  }
+  __syncthreads();
+  t.x_ready = true;
 }
 
 // ---------------------------------------------------------- one segment
-// z of one segment into ZS (all points of the tile), then barrier.
+// z of one segment for all points of the tile, then barrier; returns where
+// z lives (row stride ldz).
 template <class T>
-__device__ void stage_segment(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
-                              const rb_segment& seg) {
-  bool bad;
+__device__ const T* stage_segment(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
+                                  const rb_segment& seg, TileCtx& t) {
+  uint32_t nf = 0u;
+  const T* zb = s.ZS;
   if (seg.n_groups == 0) {                 // shift-only ids 10 and 15 (engine.py:96-104)
+    T* zw = s.ZS;
     const T* o = a.values + mem.shift;
     const int32_t* perm = mem.perm >= 0 ? a.index + mem.perm + seg.src : nullptr;
     const T scale = (T)seg.scale, pre = (T)seg.pre, post = (T)seg.post;
     const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
-    bad = false;
     for (int j = l8; j < seg.d; j += 8) {
       const int src = perm ? perm[j] : j;
       T v = scale * (s.XS[p * a.dim + src] - o[src]);
       if (pre != T(0)) v = v + pre;
       if (post != T(0)) v = v + post;
-      put_z(a, s, p, j, v, bad);
+      zw[p * a.ldz + j] = v;
+      if (not_finite(v)) nf |= 1u << p;
     }
   } else {
-    bad = rotate(a, s, seg);
+    nf = rotate(a, s, seg);
   }
-  if (bad) atomicOr(a.flag, 2);
+  if (nf & s.P->live) atomicOr(a.flag, 2);
   __syncthreads();
+  return zb;
 }
 
 // Value of one member (basic function, hybrid, or composition member) for
 // the calling lane's point.
 template <class T, int KID>
-__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem) {
+__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, TileCtx& t) {
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
   T total = T(0);
   for (int si = 0; si < mem.n_segments; ++si) {
     const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
-    stage_segment(a, s, mem, seg);
-    const Pt<T> pt{s.ZS + p * a.ldz, seg.d, l8, a.values + seg.ctab};
+    const T* zb = stage_segment(a, s, mem, seg, t);
+    const Pt<T> pt{zb + p * a.ldz, seg.d, l8, a.values + seg.ctab};
     T v;
     if constexpr (KID >= 0) v = kernel_value_k<T, KID>(pt);
     else v = kernel_value<T>(seg.kernel, pt);
     total = (si == 0) ? v : total + v;   // hybrid.py:105-115: 0 + K_0 + K_1 + ...
-    __syncthreads();                      // ZS is rewritten by the next segment
+    __syncthreads();                      // z is rewritten by the next segment
+  }
+  return total;
+}
+
+// composition.py:114-141: the normalised weights om[k] of the calling
+// lane's point (row x of the X tile) from its squared distances to every
+// member optimum: one-hot on an optimum (d2 < 1e-24), uniform if all
+// weights underflow.
+template <class T>
+__device__ __forceinline__ void composition_weights(const Args<T>& a, const PlanHead& P, const T* x,
+                                                    int l8, T (&om)[MAX_MEMBERS]) {
+  const int nm = P.fn.n_members;
+  T d2[MAX_MEMBERS];
+#pragma unroll
+  for (int k = 0; k < MAX_MEMBERS; ++k) {
+    d2[k] = T(0);
+    om[k] = T(0);
+    if (k < nm) {
+      const T* o = a.values + P.mem[k].shift;
+      d2[k] = pw8<T>(0, a.dim, [&](int j) { const T u = x[j] - o[j]; return u * u; }, l8);
+    }
+  }
+  T mn = d2[0];
+  int am = 0;
+#pragma unroll
+  for (int k = 1; k < MAX_MEMBERS; ++k)
+    if (k < nm && d2[k] < mn) { mn = d2[k]; am = k; }
+  if (mn < C<T>(1.0000000000000002e-24)) {          // 1e-12**2: on an optimum
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k) om[k] = (k == am) ? T(1) : T(0);
+  } else {
+    T w[MAX_MEMBERS], tot = T(0);
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k) {
+      w[k] = T(0);
+      if (k < nm) {
+        const T sg = (T)P.mem[k].sigma;
+        w[k] = apow<T>(d2[k], C<T>(-0.5)) *
+               M<T>::exp(-d2[k] / (C<T>(2.0 * a.dim) * (sg * sg)));
+        tot = tot + w[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k)
+      if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;
+  }
+}
+
+// composition.py:114-166 for the calling lane's point: weights from the
+// squared distances to every member optimum (X tile in XS), then the
+// sigma-weighted, biased member values, skipping zero weights.
+template <class T>
+__device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid) {
+  PlanHead& P = *s.P;
+  const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const int nm = P.fn.n_members;
+  T om[MAX_MEMBERS];
+  composition_weights<T>(a, P, s.XS + p * a.dim, l8, om);
+  // composition.py:157-166: zero weights are skipped (and not checked)
+  T total = T(0);
+#pragma unroll 1
+  for (int k = 0; k < nm; ++k) {
+    T omk = T(0);
+#pragma unroll
+    for (int kk = 0; kk < MAX_MEMBERS; ++kk)
+      if (kk == k) omk = om[kk];
+    const bool use = valid && omk != T(0);
+    __syncthreads();                                   // previous member done with P.live
+    if (threadIdx.x == 0) P.live = 0u;
+    __syncthreads();
+    if (l8 == 0 && use) atomicOr(&P.live, 1u << p);
+    if (!__syncthreads_or(use)) continue;
+    const rb_member& mem = P.mem[k];
+    const T g = member_value<T, GENERIC>(a, s, mem, t);
+    if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
   }
   return total;
 }
@@ -501,105 +683,63 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  uint32_t phase0 = 0u, phase1 = 0u;
+  TileCtx t{0, 0, 0u, false};
+  uint32_t phase1 = 0u;
   const int64_t first = blockIdx.x;
-  if (a.nbuf == 2 && threadIdx.x == 0 && first < ntiles && tile_is_bulk(a, tile_rows(a, first)))
+  const bool f64 = sizeof(T) == 8;
+  if (!f64 && a.nbuf == 2 && threadIdx.x == 0 && first < ntiles &&
+      tile_is_bulk(a, tile_rows(a, first)))
     issue_tile(a, s.XB[0], &P.mbar[0], first, tile_rows(a, first));
 
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
-    const int b = (a.nbuf == 2) ? (it & 1) : 0;
+    const int b = (!f64 && a.nbuf == 2) ? (it & 1) : 0;
     Smem<T> st = s;
     st.XS = b ? s.XB[1] : s.XB[0];
     const int64_t row0 = tile * TP;
     const int nv = tile_rows(a, tile);
+    t.tile = tile;
+    t.nv = nv;
     const uint32_t valid_mask = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
     const int64_t next = tile + gridDim.x;
     if (threadIdx.x == 0) {
-      if (a.nbuf == 2 && next < ntiles && tile_is_bulk(a, tile_rows(a, next)))
-        issue_tile(a, b ? s.XB[0] : s.XB[1], b ? &P.mbar[0] : &P.mbar[1], next,
-                   tile_rows(a, next));
-      if (a.nbuf == 1 && tile_is_bulk(a, nv)) issue_tile(a, st.XS, &P.mbar[0], tile, nv);
       P.live = valid_mask;
+      if (a.l2pf) prefetch_tile_l2(a, next + (a.nbuf == 2 ? (int64_t)gridDim.x : 0));
     }
-    if (tile_is_bulk(a, nv)) {
-      if (b) {
-        wait_tile(&P.mbar[1], phase1);
-        phase1 ^= 1u;
-      } else {
-        wait_tile(&P.mbar[0], phase0);
-        phase0 ^= 1u;
-      }
+    if constexpr (sizeof(T) == 8) {
+      fetch_x(a, st, t);          // barrier inside also publishes P.live
     } else {
-      const T* src = a.x + row0 * a.dim;
-      for (int e = threadIdx.x; e < nv * a.dim; e += NT) st.XS[e] = src[e];
+      if (threadIdx.x == 0) {
+        if (a.nbuf == 2 && next < ntiles && tile_is_bulk(a, tile_rows(a, next)))
+          issue_tile(a, b ? s.XB[0] : s.XB[1], b ? &P.mbar[0] : &P.mbar[1], next,
+                     tile_rows(a, next));
+        if (a.nbuf == 1 && tile_is_bulk(a, nv)) issue_tile(a, st.XS, &P.mbar[0], tile, nv);
+      }
+      if (tile_is_bulk(a, nv)) {
+        if (b) {
+          wait_tile(&P.mbar[1], phase1);
+          phase1 ^= 1u;
+        } else {
+          wait_tile(&P.mbar[0], t.phase);
+          t.phase ^= 1u;
+        }
+      } else {
+        const T* src = a.x + row0 * a.dim;
+        for (int e = threadIdx.x; e < nv * a.dim; e += NT) st.XS[e] = src[e];
+      }
+      __syncthreads();
+      t.x_ready = true;
     }
-    __syncthreads();
     // A non-finite x reaches some z of every evaluated member, so the z
     // checks cover the batch check of engine.py:202-203 as well.
     const bool valid = p < nv;
     T result;
     if constexpr (KID >= 0) {
-      result = member_value<T, KID>(a, st, P.mem[0]);
+      result = member_value<T, KID>(a, st, P.mem[0], t);
     } else if (P.fn.category != RB_COMPOSITION) {
-      result = member_value<T, GENERIC>(a, st, P.mem[0]);
+      result = member_value<T, GENERIC>(a, st, P.mem[0], t);
     } else {
-      // composition.py:114-141: weights from the squared distances
-      const int nm = P.fn.n_members;
-      const T* x = st.XS + p * a.dim;
-      T d2[MAX_MEMBERS], om[MAX_MEMBERS];
-#pragma unroll
-      for (int k = 0; k < MAX_MEMBERS; ++k) {
-        d2[k] = T(0);
-        om[k] = T(0);
-        if (k < nm) {
-          const T* o = a.values + P.mem[k].shift;
-          d2[k] = pw8<T>(0, a.dim, [&](int j) { const T t = x[j] - o[j]; return t * t; }, l8);
-        }
-      }
-      T mn = d2[0];
-      int am = 0;
-#pragma unroll
-      for (int k = 1; k < MAX_MEMBERS; ++k)
-        if (k < nm && d2[k] < mn) { mn = d2[k]; am = k; }
-      if (mn < C<T>(1.0000000000000002e-24)) {          // 1e-12**2: on an optimum
-#pragma unroll
-        for (int k = 0; k < MAX_MEMBERS; ++k) om[k] = (k == am) ? T(1) : T(0);
-      } else {
-        T w[MAX_MEMBERS], tot = T(0);
-#pragma unroll
-        for (int k = 0; k < MAX_MEMBERS; ++k) {
-          w[k] = T(0);
-          if (k < nm) {
-            const T sg = (T)P.mem[k].sigma;
-            w[k] = apow<T>(d2[k], C<T>(-0.5)) *
-                   M<T>::exp(-d2[k] / (C<T>(2.0 * a.dim) * (sg * sg)));
-            tot = tot + w[k];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < MAX_MEMBERS; ++k)
-          if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;
-      }
-      // composition.py:157-166: zero weights are skipped (and not checked)
-      T total = T(0);
-#pragma unroll 1
-      for (int k = 0; k < nm; ++k) {
-        T omk = T(0);
-#pragma unroll
-        for (int kk = 0; kk < MAX_MEMBERS; ++kk)
-          if (kk == k) omk = om[kk];
-        const bool use = valid && omk != T(0);
-        __syncthreads();                                   // previous member done with P.live
-        if (threadIdx.x == 0) P.live = 0u;
-        __syncthreads();
-        if (l8 == 0 && use) atomicOr(&P.live, 1u << p);
-        if (!__syncthreads_or(use)) continue;
-        const rb_member& mem = P.mem[k];
-        const T g = member_value<T, GENERIC>(a, st, mem);
-        if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
-      }
-      result = total;
+      result = composition_value<T>(a, st, t, valid);
     }
     if (l8 == 0 && valid) a.f[row0 + p] = result + C<T>(100.0);     // engine.py:209
     __syncthreads();                                                 // XS reused by next TMA

@@ -30,7 +30,7 @@ import numpy as np
 from . import catalog, instances
 
 GROUP_DT = np.dtype([("m", "<i4"), ("qb", "<i4", (10,)), ("col", "<i4"),
-                     ("row", "<i4"), ("mat", "<i4"), ("frag", "<i4"), ("reserved", "<i4")])
+                     ("row", "<i4"), ("mat", "<i4"), ("frag", "<i4"), ("cz", "<i4")])
 SEGMENT_DT = np.dtype({
     "names": ["kernel", "d", "src", "n_groups", "group0", "ctab", "scale", "pre", "post"],
     "formats": ["<i4"] * 6 + ["<f8"] * 3,
@@ -114,9 +114,15 @@ class _Builder:
         return off
 
     # -- descriptors
-    def group(self, block: np.ndarray, cols, rows, n: int) -> int:
+    def group(self, block: np.ndarray, cols, rows, n: int, scale: float, pre: float,
+              post: float) -> int:
         """One rotation block acting on positions ``cols`` of a length-n
-        segment vector and writing positions ``rows`` of z."""
+        segment vector and writing positions ``rows`` of z.
+
+        float64 rotate algebra: z = R(scale (x - o) + pre) + post
+        = (scale R)(x - o) - cz with cz_r = -pre sum_q R[r, q] - post, so the
+        DMMA fragments hold scale * block and x - o stays an exact zero at
+        the optimum (z is then exactly post, as in the reference)."""
         m = block.shape[0]
         cols = [int(c) for c in cols]
         order = sorted(range(m), key=lambda k: (slot_of(cols[k], n), cols[k]))
@@ -137,7 +143,9 @@ class _Builder:
         rec["col"] = self.ints([cols[k] for k in order])
         rec["row"] = self.ints(rows)
         rec["mat"] = self.values(padded[:m, :m4])
-        rec["frag"] = self.values(frag)
+        rec["frag"] = self.values(scale * frag, frag.astype(np.float32))
+        cz = -np.longdouble(pre) * mat.astype(np.longdouble).sum(axis=0) - np.longdouble(post)
+        rec["cz"] = self.values(cz.astype(np.float64))
         self.groups.append(rec)
         return len(self.groups) - 1
 
@@ -146,7 +154,7 @@ class _Builder:
         scale, pre, post = catalog.KERNEL_PIPELINE[kernel]
         g0 = len(self.groups)
         for blk, cols, rows in blocks:
-            self.group(blk, cols, rows, d)
+            self.group(blk, cols, rows, d, scale, pre, post)
         if blocks:
             self.max_exact_len = max(self.max_exact_len, d)
             self.max_q = max(self.max_q, sum((b.shape[0] + 3) // 4 * 4 for b, _, _ in blocks))

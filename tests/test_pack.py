@@ -93,9 +93,17 @@ def test_pack_shapes_and_disabled():
     assert pk100.max_exact_len == 100
 
 
+def _segment_of_group(pk, gi):
+    for seg in pk.segments:
+        if seg["group0"] <= gi < seg["group0"] + seg["n_groups"]:
+            return seg
+    raise AssertionError(gi)
+
+
 def test_dmma_fragments_match_q_ordered_block():
     pk = P.Pack(100, 0)
-    for g in pk.groups[:6]:
+    for gi, g in enumerate(pk.groups[:12]):
+        scale = float(_segment_of_group(pk, gi)["scale"])
         m = int(g["m"])
         nt, nk, m4 = (m + 7) // 8, (m + 3) // 4, (m + 3) // 4 * 4
         mat = pk.values_f64[g["mat"]:g["mat"] + m * m4].reshape(m, m4)
@@ -104,9 +112,38 @@ def test_dmma_fragments_match_q_ordered_block():
             for ks in range(nk):
                 for lane in range(32):
                     q, r = 4 * ks + lane % 4, 8 * a + lane // 4
-                    want = mat[q, r] if (q < m and r < m) else 0.0
+                    want = scale * mat[q, r] if (q < m and r < m) else 0.0
                     assert frag[a, ks, lane] == want
         assert g["mat"] % 4 == 0 and g["frag"] % 4 == 0
+
+
+@pytest.mark.parametrize("dim", [2, 3, 10, 13, 50, 100])
+def test_fp64_offsets_restate_the_transform(dim):
+    """(scale B)(x - o)[src] - cz == R(scale (x - o)[src] + pre) + post for
+    every rotated segment of every member (the float64 rotate's algebra),
+    and exactly post at the optimum."""
+    pk = P.Pack(dim, 0, disabled=frozenset(range(23, 37)) if dim < 10 else frozenset())
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-100, 100, dim)
+    for mem in pk.members:
+        o = pk.values_f64[mem["shift"]:mem["shift"] + dim]
+        perm = (pk.index[mem["perm"]:mem["perm"] + dim] if mem["perm"] >= 0 else None)
+        for si in range(mem["segment0"], mem["segment0"] + mem["n_segments"]):
+            seg = pk.segments[si]
+            for gi in range(seg["group0"], seg["group0"] + seg["n_groups"]):
+                g = pk.groups[gi]
+                m = int(g["m"])
+                m4 = (m + 3) // 4 * 4
+                mat = pk.values_f64[g["mat"]:g["mat"] + m * m4].reshape(m, m4)[:, :m]
+                pos = pk.index[g["col"]:g["col"] + m] + seg["src"]
+                src = perm[pos] if perm is not None else pos
+                v = seg["scale"] * (x[src] - o[src]) + seg["pre"]
+                want = mat.T @ v + seg["post"]
+                cz = pk.values_f64[g["cz"]:g["cz"] + m]
+                got = (seg["scale"] * mat).T @ (x[src] - o[src]) - cz
+                assert np.allclose(got, want, rtol=1e-12, atol=1e-10 * max(1.0, np.abs(want).max()))
+                if seg["pre"] == 0.0:
+                    assert np.all(-cz == seg["post"])
 
 
 def test_kernel_constants_follow_numpy():
