@@ -142,6 +142,11 @@ int64_t rb_launch_count(void);
  * semantics (bit-exact SVML powf restatement, csrc/rb_svml_powf.cuh), on
  * device pointers; synchronous on `stream`. */
 rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void* stream);
+/* Diagnostic: clock64() sums of the evaluation kernels of one precision
+ * (0 = float64, 1 = float32) over CTAs: [0] tile load, [1] z staging
+ * (rotate), [2] kernel values, [3] whole tiles, [4] tiles; zeros unless the
+ * library is built with -DRB_PHASE_TIMING.  reset != 0 clears them. */
+void rb_debug_phases(int32_t precision, uint64_t out[8], int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,8 @@ _STATUS = {
 
 EXPORTS = ("rb_initialize", "rb_dispose", "rb_func_evaluate", "rb_func_evaluatef",
            "rb_h_func_evaluate", "rb_h_func_evaluatef", "rb_last_error",
-           "rb_abi_version", "rb_struct_sizes", "rb_launch_count", "rb_np_powf")
+           "rb_abi_version", "rb_struct_sizes", "rb_launch_count", "rb_np_powf",
+           "rb_debug_phases")
 
 
 class RbPack(ctypes.Structure):
@@ -76,6 +77,8 @@ def load() -> ctypes.CDLL:
     lib.rb_launch_count.restype = i64
     lib.rb_np_powf.argtypes = [vp, vp, vp, i64, vp]
     lib.rb_np_powf.restype = i32
+    lib.rb_debug_phases.argtypes = [i32, ctypes.POINTER(ctypes.c_uint64), i32]
+    lib.rb_debug_phases.restype = None
     _check_layout(lib)
     _lib = lib
     return lib
@@ -115,3 +118,10 @@ def make_pack(p: pack.Pack) -> RbPack:
 
 def launch_count() -> int:
     return int(load().rb_launch_count())
+
+
+def debug_phases(precision: str, reset: bool = True) -> list[int]:
+    """Phase clock sums (diagnostic builds with -DRB_PHASE_TIMING)."""
+    out = (ctypes.c_uint64 * 8)()
+    load().rb_debug_phases(0 if precision == "double" else 1, out, int(reset))
+    return list(out)

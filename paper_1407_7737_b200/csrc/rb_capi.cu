@@ -17,6 +17,8 @@ extern const void* const kernels_f64[N_VARIANTS];
 extern const void* const kernels_f32[N_VARIANTS];
 cudaError_t set_weier_f64(const double* a_then_c);
 cudaError_t set_weier_f32(const float* a_then_c);
+void phase_read_f64(unsigned long long out[8], bool reset);
+void phase_read_f32(unsigned long long out[8], bool reset);
 
 __global__ void np_powf_kernel(const float* x, const float* y, float* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -65,6 +67,7 @@ struct Launch {
   int grid_cap = 0;
   int ldv = 0, max_q = 0;
   int nbuf = 1;
+  int opt_rows = 0;
   size_t smem_nbuf[3] = {0, 0, 0};
 };
 
@@ -177,6 +180,7 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
   a.nbuf = L.nbuf;
   a.l2pf = l2_prefetch();
+  a.opt_rows = L.opt_rows;
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
   void* args[] = {&a};
@@ -268,9 +272,10 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       L.func = (pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[variant[fi]];
       L.max_q = std::max(max_q, 1);
       L.ldv = ldv;
+      L.opt_rows = fn.category == RB_COMPOSITION ? fn.n_members : 0;
       for (int nb = 1; nb <= 2; ++nb)
-        L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, L.ldv, e->ldz[0], L.max_q, nb)
-                                  : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q, nb);
+        L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, L.ldv, e->ldz[0], L.max_q, nb, L.opt_rows)
+                                  : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q, nb, L.opt_rows);
       if ((int)L.smem_nbuf[1] > optin)
         return fail(RB_E_UNSUPPORTED, "dimension too large for the shared-memory tile");
       const size_t top = (int)L.smem_nbuf[2] <= optin ? L.smem_nbuf[2] : L.smem_nbuf[1];
@@ -336,6 +341,17 @@ int32_t rb_abi_version(void) { return 1; }
 const char* rb_last_error(void) { return g_last_error.c_str(); }
 
 int64_t rb_launch_count(void) { return g_launches.load(); }
+
+/* Diagnostics (not part of the reference interface): per-phase clock sums
+ * of the evaluation kernels of one precision (0 = float64, 1 = float32):
+ * [load, stage, kernel, tile, tiles] summed over CTAs; zeros unless the
+ * library was built with -DRB_PHASE_TIMING (tools/phase_timing.py). */
+void rb_debug_phases(int32_t precision, uint64_t out[8], int32_t reset) {
+  unsigned long long v[8];
+  if (precision == 0) rb::phase_read_f64(v, reset != 0);
+  else rb::phase_read_f32(v, reset != 0);
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+}
 
 void rb_struct_sizes(int64_t out[5]) {
   out[0] = sizeof(rb_group);

@@ -44,6 +44,17 @@ namespace rb {
 #define RB_TP 32
 #endif
 constexpr int TP = RB_TP;       // points per tile (16 or 32)
+
+// Optional phase timing (tools/phase_timing.py): thread 0 of every CTA adds
+// the clock64() spent per tile in load / z staging / kernel phases.
+#ifdef RB_PHASE_TIMING
+static __device__ unsigned long long g_phase[8];
+#define RB_PHASE_MARK(var) const long long var = clock64()
+#define RB_PHASE_ADD(i, dt) if (threadIdx.x == 0) atomicAdd(&g_phase[i], (unsigned long long)(dt))
+#else
+#define RB_PHASE_MARK(var)
+#define RB_PHASE_ADD(i, dt)
+#endif
 constexpr int NT = 8 * TP;      // threads per CTA = 8 lanes x TP
 constexpr int NWARPS = NT / 32;
 constexpr int MAX_MEMBERS = 5;
@@ -51,6 +62,10 @@ constexpr int MAX_SEGMENTS = 16;
 constexpr int MAX_GROUPS = 16;
 constexpr int MAX_UNITS = 512;  // fp64 DMMA units (m-tile x n-tile of a group) per function
 constexpr int NTC = RB_NTC;     // DMMA n-tiles (8 rows) accumulated per pass
+#ifndef RB_KB
+#define RB_KB 1
+#endif
+constexpr int KB = RB_KB;       // fp64 rotate: k-steps whose operands are loaded ahead
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
 template <class T>
@@ -73,6 +88,7 @@ struct Args {
   int tma;          // x is 16-byte aligned: bulk-copy full tiles
   int nbuf;         // 2: prefetch the next tile while computing this one
   int l2pf;         // 1: also pull the tile after the next in-flight one into L2
+  int opt_rows;     // member optima staged in shared memory (compositions)
 };
 
 struct PlanHead {
@@ -103,6 +119,7 @@ struct Smem {
   int* prow;      // z position of the group's r-th block row
   T* qo;          // the optimum at the q-th column
   T* cz;          // fp64: offset constant of the r-th block row (pack.py group())
+  T* opt;         // compositions: member optima [n_members][dim]
   T* XS;          // [TP][dim], the current tile (one of XB)
   T* XB[2];       // X tile buffers (XB[1] == XB[0] without prefetch)
   T* VS;          // fp32 only: [ldv][TP]
@@ -114,10 +131,12 @@ __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(
 __host__ __device__ inline int imax(int a, int b) { return a > b ? a : b; }
 
 template <class T>
-__host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q, int nbuf) {
+__host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_q, int nbuf,
+                                             int opt_rows) {
   size_t b = align16(sizeof(PlanHead));
   b += 2 * align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
   if (sizeof(T) == 8) b += align16(sizeof(T) * max_q);
+  b += align16(sizeof(T) * opt_rows * dim);
   b += nbuf * align16(sizeof(T) * TP * dim);
   if (sizeof(T) == 4) b += align16(sizeof(T) * TP * ldv);
   b += align16(sizeof(T) * TP * ldz);
@@ -141,6 +160,8 @@ __device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
     s.cz = reinterpret_cast<T*>(base + off);
     off += align16(sizeof(T) * a.max_q);
   }
+  s.opt = reinterpret_cast<T*>(base + off);
+  off += align16(sizeof(T) * a.opt_rows * a.dim);
   s.XB[0] = reinterpret_cast<T*>(base + off);
   off += align16(sizeof(T) * TP * a.dim);
   s.XB[1] = s.XB[0];
@@ -216,6 +237,8 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
     P.unit_off[P.n_seg] = nu;
   }
   __syncthreads();
+  for (int mi = 0; mi < a.opt_rows && mi < P.fn.n_members; ++mi)
+    for (int j = threadIdx.x; j < a.dim; j += nth) s.opt[mi * a.dim + j] = a.values[P.mem[mi].shift + j];
   for (int mi = 0; mi < P.fn.n_members; ++mi) {
     const rb_member& mem = P.mem[mi];
     const T* o = a.values + mem.shift;
@@ -310,12 +333,17 @@ __device__ __forceinline__ bool not_finite(float v) {
 
 // z value into ZS; records point p in `nf` when the value is not finite
 // (kernels.py:45-49).  stage_segment masks nf with the live points.
-template <class T>
+template <bool CHECK, class T>
 __device__ __forceinline__ void put_z(const Args<T>& a, const Smem<T>& s, int p, int pos, T v,
                                       uint32_t& nf) {
   s.ZS[p * a.ldz + pos] = v;
-  if (not_finite(v)) nf |= 1u << p;
+  if (CHECK && not_finite(v)) nf |= 1u << p;
 }
+
+// |x| bound below which z = R(scale (x - o) + pre) + post cannot overflow
+// (|scale| <= 10, rows of R have unit norm, D < 10^6): 2^960 in float64,
+// 2^100 in float32.  Tiles whose x all lie below it skip the per-z
+// finiteness test, which the X scan in evaluate_kernel then proves.
 
 // ------------------------------------------------------------ rotate fp64
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b) {
@@ -339,7 +367,7 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
 // n-tiles sharing (group, m-tile), so one A fragment per k-step feeds the
 // run.  Fragment layouts (PTX m16n8k4 .f64): a_i = (gid + 8i, tig),
 // b = (tig, gid), c_i = (gid + 8*(i>>1), 2*tig + (i&1)).
-template <int NW>
+template <int NW, bool CHECK>
 __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int si,
                                       int warp) {
   const PlanHead& P = *s.P;
@@ -365,15 +393,29 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
     for (int c = 0; c < NTC; ++c)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[c][i] = 0.0;
-#pragma unroll 3
-    for (int ks = 0; ks < nks; ++ks) {
-      const int col = qs[ks * 4];
-      const double o = qo[ks * 4];
-      const double a0 = X0[col] - o;
-      const double a1 = X1[col] - o;
+    // k-steps in batches of KB: the batch's gathers and B loads issue before
+    // its DMMAs, so one load latency is paid per batch, not per k-step
+    for (int k0 = 0; k0 < nks; k0 += KB) {
+      double fa0[KB], fa1[KB], fb[KB][NTC];
 #pragma unroll
-      for (int c = 0; c < NTC; ++c)
-        if (c < run) dmma_16x8x4(acc[c], a0, a1, __ldg(F + (c * nks + ks) * 32));
+      for (int k = 0; k < KB; ++k) {
+        if (k0 + k < nks) {
+          const int col = qs[(k0 + k) * 4];
+          const double o = qo[(k0 + k) * 4];
+          fa0[k] = X0[col] - o;
+          fa1[k] = X1[col] - o;
+#pragma unroll
+          for (int c = 0; c < NTC; ++c)
+            if (c < run) fb[k][c] = __ldg(F + (c * nks + k0 + k) * 32);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if (k0 + k < nks) {
+#pragma unroll
+          for (int c = 0; c < NTC; ++c)
+            if (c < run) dmma_16x8x4(acc[c], fa0[k], fa1[k], fb[k][c]);
+        }
     }
     const int* prow = s.prow + P.gq0[g];
     const double* cz = s.cz + P.gq0[g];
@@ -388,26 +430,30 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
         if (rr < m) {
           const double zv = acc[c][i] - cz[rr];
           s.ZS[(p0 + ((i >> 1) << 3)) * a.ldz + prow[rr]] = zv;
-          const uint32_t e = (uint32_t)__double2hiint(zv) & 0x7ff00000u;
-          if (i < 2) e0 = max(e0, e); else e1 = max(e1, e);
+          if (CHECK) {
+            const uint32_t e = (uint32_t)__double2hiint(zv) & 0x7ff00000u;
+            if (i < 2) e0 = max(e0, e); else e1 = max(e1, e);
+          }
         }
       }
     }
-    if (e0 == 0x7ff00000u) nf |= 1u << p0;      // NaN or infinity (kernels.py:45-49)
-    if (e1 == 0x7ff00000u) nf |= 1u << (p0 + 8);
+    if (CHECK && e0 == 0x7ff00000u) nf |= 1u << p0;      // NaN or infinity (kernels.py:45-49)
+    if (CHECK && e1 == 0x7ff00000u) nf |= 1u << (p0 + 8);
     u += run;
   }
   return nf;
 }
 
+template <bool CHECK>
 __device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
-  return rotate_f64<NWARPS>(a, s, (int)(&seg - s.P->seg), threadIdx.x >> 5);
+  return rotate_f64<NWARPS, CHECK>(a, s, (int)(&seg - s.P->seg), threadIdx.x >> 5);
 }
 
 // ------------------------------------------------------------ rotate fp32
 // Exact NumPy order (transforms.py:42-48): rounded products, per-slot
 // accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
 // ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
+template <bool CHECK>
 __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
   const PlanHead& P = *s.P;
   const int g0 = seg.group0 - P.grp_base;
@@ -510,7 +556,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, co
         const int row = prow[r0 + j];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          put_z(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j], nf);
+          put_z<CHECK>(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j], nf);
       }
     }
   }
@@ -523,7 +569,8 @@ struct TileCtx {
   int64_t tile;
   int nv;             // valid rows
   uint32_t phase;     // parity of mbar[0] (fp64 loads / refetches)
-  bool x_ready;       // fp64: buffer A holds the X tile (not a segment's z)
+  bool x_ready;       // XS holds the X tile
+  bool check_z;       // some valid x of the tile is huge or not finite: test every z
 };
 
 // X tile into XS (buffer A for fp64); all threads; ends with a barrier.
@@ -563,10 +610,10 @@ __device__ const T* stage_segment(const Args<T>& a, const Smem<T>& s, const rb_m
       if (pre != T(0)) v = v + pre;
       if (post != T(0)) v = v + post;
       zw[p * a.ldz + j] = v;
-      if (not_finite(v)) nf |= 1u << p;
+      if (t.check_z && not_finite(v)) nf |= 1u << p;
     }
   } else {
-    nf = rotate(a, s, seg);
+    nf = t.check_z ? rotate<true>(a, s, seg) : rotate<false>(a, s, seg);
   }
   if (nf & s.P->live) atomicOr(a.flag, 2);
   __syncthreads();
@@ -582,13 +629,18 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
   T total = T(0);
   for (int si = 0; si < mem.n_segments; ++si) {
     const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
+    RB_PHASE_MARK(c0);
     const T* zb = stage_segment(a, s, mem, seg, t);
+    RB_PHASE_MARK(c1);
     const Pt<T> pt{zb + p * a.ldz, seg.d, l8, a.values + seg.ctab};
     T v;
     if constexpr (KID >= 0) v = kernel_value_k<T, KID>(pt);
     else v = kernel_value<T>(seg.kernel, pt);
     total = (si == 0) ? v : total + v;   // hybrid.py:105-115: 0 + K_0 + K_1 + ...
     __syncthreads();                      // z is rewritten by the next segment
+    RB_PHASE_MARK(c2);
+    RB_PHASE_ADD(1, c1 - c0);
+    RB_PHASE_ADD(2, c2 - c1);
   }
   return total;
 }
@@ -599,7 +651,7 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
 // weights underflow.
 template <class T>
 __device__ __forceinline__ void composition_weights(const Args<T>& a, const PlanHead& P, const T* x,
-                                                    int l8, T (&om)[MAX_MEMBERS]) {
+                                                    const T* opt, int l8, T (&om)[MAX_MEMBERS]) {
   const int nm = P.fn.n_members;
   T d2[MAX_MEMBERS];
 #pragma unroll
@@ -607,7 +659,7 @@ __device__ __forceinline__ void composition_weights(const Args<T>& a, const Plan
     d2[k] = T(0);
     om[k] = T(0);
     if (k < nm) {
-      const T* o = a.values + P.mem[k].shift;
+      const T* o = opt + k * a.dim;
       d2[k] = pw8<T>(0, a.dim, [&](int j) { const T u = x[j] - o[j]; return u * u; }, l8);
     }
   }
@@ -626,8 +678,9 @@ __device__ __forceinline__ void composition_weights(const Args<T>& a, const Plan
       w[k] = T(0);
       if (k < nm) {
         const T sg = (T)P.mem[k].sigma;
-        w[k] = apow<T>(d2[k], C<T>(-0.5)) *
-               M<T>::exp(-d2[k] / (C<T>(2.0 * a.dim) * (sg * sg)));
+        // d2 ** -0.5: float64 to tolerance via rsqrt; float32 NumPy's SVML powf
+        const T ih = sizeof(T) == 8 ? (T)::rsqrt((double)d2[k]) : apow<T>(d2[k], C<T>(-0.5));
+        w[k] = ih * M<T>::exp(-d2[k] / (C<T>(2.0 * a.dim) * (sg * sg)));
         tot = tot + w[k];
       }
     }
@@ -646,7 +699,7 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int nm = P.fn.n_members;
   T om[MAX_MEMBERS];
-  composition_weights<T>(a, P, s.XS + p * a.dim, l8, om);
+  composition_weights<T>(a, P, s.XS + p * a.dim, s.opt, l8, om);
   // composition.py:157-166: zero weights are skipped (and not checked)
   T total = T(0);
 #pragma unroll 1
@@ -683,7 +736,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  TileCtx t{0, 0, 0u, false};
+  TileCtx t{0, 0, 0u, false, false};
   uint32_t phase1 = 0u;
   const int64_t first = blockIdx.x;
   const bool f64 = sizeof(T) == 8;
@@ -696,6 +749,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     const int b = (!f64 && a.nbuf == 2) ? (it & 1) : 0;
     Smem<T> st = s;
     st.XS = b ? s.XB[1] : s.XB[0];
+    RB_PHASE_MARK(c_tile);
     const int64_t row0 = tile * TP;
     const int nv = tile_rows(a, tile);
     t.tile = tile;
@@ -730,9 +784,25 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
       __syncthreads();
       t.x_ready = true;
     }
-    // A non-finite x reaches some z of every evaluated member, so the z
-    // checks cover the batch check of engine.py:202-203 as well.
+    // engine.py:202-203: a non-finite x anywhere in the batch raises; a
+    // finite but huge x can still overflow z (kernels.py:45-49), so such
+    // tiles test every z they produce.
     const bool valid = p < nv;
+    {
+      // max of |x| bit patterns (high word for float64) over the point's row
+      uint32_t mx = 0u;
+      if (valid) {
+        const uint32_t* xw = reinterpret_cast<const uint32_t*>(st.XS + p * a.dim);
+        constexpr int W = sizeof(T) / 4;          // 32-bit words per element
+#pragma unroll 4
+        for (int j = l8; j < a.dim; j += 8) mx = max(mx, xw[j * W + W - 1] & 0x7fffffffu);
+      }
+      const bool big = sizeof(T) == 8 ? mx >= 0x7bf00000u : mx >= 0x71800000u;   // x_large
+      if (sizeof(T) == 8 ? mx >= 0x7ff00000u : mx >= 0x7f800000u) atomicOr(a.flag, 2);
+      t.check_z = __syncthreads_or(big) != 0;
+    }
+    RB_PHASE_MARK(c_loaded);
+    RB_PHASE_ADD(0, c_loaded - c_tile);
     T result;
     if constexpr (KID >= 0) {
       result = member_value<T, KID>(a, st, P.mem[0], t);
@@ -743,6 +813,9 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     }
     if (l8 == 0 && valid) a.f[row0 + p] = result + C<T>(100.0);     // engine.py:209
     __syncthreads();                                                 // XS reused by next TMA
+    RB_PHASE_MARK(c_end);
+    RB_PHASE_ADD(3, c_end - c_tile);
+    RB_PHASE_ADD(4, 1);
   }
 }
 

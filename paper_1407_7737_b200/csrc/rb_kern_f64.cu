@@ -25,4 +25,18 @@ cudaError_t set_weier_f64(const double* a_then_c) {
   return cudaMemcpyToSymbol(kWei64, a_then_c, sizeof(WeierTab<double>));
 }
 
+// Phase timing counters of this unit (zeros unless built with RB_PHASE_TIMING).
+void phase_read_f64(unsigned long long out[8], bool reset) {
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+#ifdef RB_PHASE_TIMING
+  cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  }
+#else
+  (void)reset;
+#endif
+}
+
 }  // namespace rb

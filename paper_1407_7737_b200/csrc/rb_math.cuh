@@ -155,16 +155,50 @@ __device__ __noinline__ T pw8_tree(int lo, int n, F& f, int l8) {
   return val;
 }
 
+// float64 sums: the bar is 1e-12 relative, not NumPy's bits, so each lane
+// keeps two independent partial sums (ILP) over its strided elements and
+// the 8 lane partials meet in an xor butterfly.  The order is fixed per
+// point (bit-identical across batches and tiles).
+template <class F>
+__device__ __forceinline__ double sum8_f64(int lo, int n, F& f, int l8) {
+  double r0 = 0.0, r1 = 0.0;
+  int i = l8;
+#pragma unroll 2
+  for (; i + 8 < n; i += 16) {
+    r0 = r0 + f(lo + i);
+    r1 = r1 + f(lo + i + 8);
+  }
+  if (i < n) r0 = r0 + f(lo + i);
+  double r = r0 + r1;
+  r = r + __shfl_xor_sync(RB_FULL, r, 1, 8);
+  r = r + __shfl_xor_sync(RB_FULL, r, 2, 8);
+  r = r + __shfl_xor_sync(RB_FULL, r, 4, 8);
+  return r;
+}
+
 template <class T, class F>
 __device__ __forceinline__ T pw8(int lo, int n, F&& f, int l8) {
-  if (n <= 128) return pw8_leaf<T>(lo, n, f, l8);
-  return pw8_tree<T>(lo, n, f, l8);
+  if constexpr (sizeof(T) == 8) {
+    return sum8_f64(lo, n, f, l8);
+  } else {
+    if (n <= 128) return pw8_leaf<T>(lo, n, f, l8);
+    return pw8_tree<T>(lo, n, f, l8);
+  }
 }
 
 // Sequential product over i = 0..n-1 of f(i) (np.prod is a plain left fold,
-// kernels.py:112); lane l8 evaluates the i = l8 (mod 8) factors.
+// kernels.py:112); lane l8 evaluates the i = l8 (mod 8) factors.  float64
+// multiplies lane partials instead (order-free to its tolerance).
 template <class T, class F>
 __device__ __forceinline__ T prod8(int n, F&& f, int l8) {
+  if constexpr (sizeof(T) == 8) {        // float64: lane partial products, butterfly
+    double q = 1.0;
+    for (int i = l8; i < n; i += 8) q = q * f(i);
+    q = q * __shfl_xor_sync(RB_FULL, q, 1, 8);
+    q = q * __shfl_xor_sync(RB_FULL, q, 2, 8);
+    q = q * __shfl_xor_sync(RB_FULL, q, 4, 8);
+    return q;
+  }
   T p = T(1);
   for (int base = 0; base < n; base += 8) {
     const int cnt = min(8, n - base);
