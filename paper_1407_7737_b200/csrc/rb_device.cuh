@@ -99,7 +99,8 @@ struct PlanHead {
   rb_group grp[MAX_GROUPS];
   int gq0[MAX_GROUPS];            // group g's slice of the per-column tables (8-aligned)
   unsigned long long mbar[2];     // TMA completion barriers, one per X buffer
-  uint32_t live;                  // points of the tile whose kernel inputs are checked
+  uint32_t live;                  // valid points of the current tile
+  uint32_t livek[MAX_MEMBERS];    // compositions: valid points with a nonzero weight, per member
   int n_jobs;                     // (member, segment) pairs per tile, in evaluation order
   int8_t job_mem[MAX_SEGMENTS];
   int8_t job_seg[MAX_SEGMENTS];   // index into seg[]
@@ -571,6 +572,7 @@ struct TileCtx {
   uint32_t phase;     // parity of mbar[0] (fp64 loads / refetches)
   bool x_ready;       // XS holds the X tile
   bool check_z;       // some valid x of the tile is huge or not finite: test every z
+  uint32_t live;      // points whose z of the current member are checked
 };
 
 // X tile into XS (buffer A for fp64); all threads; ends with a barrier.
@@ -615,7 +617,7 @@ __device__ const T* stage_segment(const Args<T>& a, const Smem<T>& s, const rb_m
   } else {
     nf = t.check_z ? rotate<true>(a, s, seg) : rotate<false>(a, s, seg);
   }
-  if (nf & s.P->live) atomicOr(a.flag, 2);
+  if (nf & t.live) atomicOr(a.flag, 2);
   __syncthreads();
   return zb;
 }
@@ -700,7 +702,15 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
   const int nm = P.fn.n_members;
   T om[MAX_MEMBERS];
   composition_weights<T>(a, P, s.XS + p * a.dim, s.opt, l8, om);
-  // composition.py:157-166: zero weights are skipped (and not checked)
+  // composition.py:157-166: zero weights are skipped (and not checked):
+  // member k runs for the tile's points with a nonzero weight (P.livek[k],
+  // zeroed at the tile start) and is skipped when there are none
+  if (l8 == 0 && valid) {
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k)
+      if (k < nm && om[k] != T(0)) atomicOr(&P.livek[k], 1u << p);
+  }
+  __syncthreads();
   T total = T(0);
 #pragma unroll 1
   for (int k = 0; k < nm; ++k) {
@@ -708,12 +718,8 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
 #pragma unroll
     for (int kk = 0; kk < MAX_MEMBERS; ++kk)
       if (kk == k) omk = om[kk];
-    const bool use = valid && omk != T(0);
-    __syncthreads();                                   // previous member done with P.live
-    if (threadIdx.x == 0) P.live = 0u;
-    __syncthreads();
-    if (l8 == 0 && use) atomicOr(&P.live, 1u << p);
-    if (!__syncthreads_or(use)) continue;
+    t.live = P.livek[k];
+    if (!t.live) continue;
     const rb_member& mem = P.mem[k];
     const T g = member_value<T, GENERIC>(a, s, mem, t);
     if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  TileCtx t{0, 0, 0u, false, false};
+  TileCtx t{0, 0, 0u, false, false, 0u};
   uint32_t phase1 = 0u;
   const int64_t first = blockIdx.x;
   const bool f64 = sizeof(T) == 8;
@@ -756,8 +762,11 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     t.nv = nv;
     const uint32_t valid_mask = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
     const int64_t next = tile + gridDim.x;
+    t.live = valid_mask;
     if (threadIdx.x == 0) {
       P.live = valid_mask;
+#pragma unroll
+      for (int k = 0; k < MAX_MEMBERS; ++k) P.livek[k] = 0u;
       if (a.l2pf) prefetch_tile_l2(a, next + (a.nbuf == 2 ? (int64_t)gridDim.x : 0));
     }
     if constexpr (sizeof(T) == 8) {

@@ -49,17 +49,41 @@ template <class T> __device__ __forceinline__ T f6_link(T x, T y) {
   const T q = x * x + y * y;
   return (sq(M<T>::sin(M<T>::sqrt(q))) - C<T>(0.5)) / sq(C<T>(1.0) + C<T>(0.001) * q) + C<T>(0.5);
 }
-// schwefel_g1 (:152-165): the branch np.where selects
+// np.mod(u, 500) for u > 0 (floored == truncated for positive operands):
+// q = trunc(u / 500) corrected by one step, then u - 500 q is exact
+// (Sterbenz: 500 q lies within [u/2, u]).  Huge u keeps libm's fmod.
+template <class T> __device__ __forceinline__ T mod500(T u) {
+  const T big = sizeof(T) == 8 ? T(1099511627776.0) : T(1048576.0);   // 2^40 / 2^20
+  if (!(u < big)) return M<T>::fmod(u, C<T>(500.0));
+  T q = M<T>::trunc(u * C<T>(0.002));
+  T r = M<T>::fma(C<T>(-500.0), q, u);
+  if (r < T(0)) {
+    q = q - T(1);
+    r = M<T>::fma(C<T>(-500.0), q, u);
+  } else if (r >= C<T>(500.0)) {
+    q = q + T(1);
+    r = M<T>::fma(C<T>(-500.0), q, u);
+  }
+  return r;
+}
+// schwefel_g1 (:152-165): the branch np.where selects, evaluated once: every
+// branch is "mult * sin(sqrt(arg)) - pen" with the reference's own operands
+//   |w| <= 500: w * sin(sqrt(|w|))
+//   w > 500:    top * sin(sqrt(top)) - (w - 500)**2 / (10000 d),   top = 500 - mod(w, 500)
+//   w < -500:   (rem - 500) * sin(sqrt(500 - rem)) - (w + 500)**2 / (10000 d),
+//               rem = mod(-w, 500)
+// so a warp runs one sin and one sqrt per element whatever the branch mix.
 template <class T> __device__ __forceinline__ T schwefel_g1(T w, T c10000d) {
   const T aw = M<T>::fabs(w);
-  if (aw <= C<T>(500.0)) return w * M<T>::sin(M<T>::sqrt(aw));
-  if (w > C<T>(500.0)) {
-    const T top = C<T>(500.0) - M<T>::fmod(w, C<T>(500.0));
-    return top * M<T>::sin(M<T>::sqrt(top)) - sq(w - C<T>(500.0)) / c10000d;
-  }
-  const T rem = M<T>::fmod(-w, C<T>(500.0));
-  return (rem - C<T>(500.0)) * M<T>::sin(M<T>::sqrt(C<T>(500.0) - rem)) -
-         sq(w + C<T>(500.0)) / c10000d;
+  const T r = mod500(aw);                              // mod(w) or mod(-w), |w| > 500
+  const bool mid = aw <= C<T>(500.0);
+  const bool high = w > C<T>(500.0);
+  const T arg = mid ? aw : C<T>(500.0) - r;            // top == 500 - rem
+  const T mult = mid ? w : (high ? arg : r - C<T>(500.0));
+  const T e = high ? w - C<T>(500.0) : w + C<T>(500.0);
+  const T pen = mid ? T(0) : sq(e) / c10000d;
+  const T v = mult * M<T>::sin(M<T>::sqrt(arg));
+  return mid ? v : v - pen;
 }
 // katsuura row sum over i = 1..32 (:178-180) for one coordinate: 8
 // accumulators in NumPy order (32 is a multiple of 8: no tail)

@@ -33,6 +33,8 @@ template <> struct M<double> {
   static __device__ __forceinline__ double floor(double x) { return ::floor(x); }
   static __device__ __forceinline__ double fabs(double x) { return ::fabs(x); }
   static __device__ __forceinline__ double fmod(double x, double y) { return ::fmod(x, y); }
+  static __device__ __forceinline__ double trunc(double x) { return ::trunc(x); }
+  static __device__ __forceinline__ double fma(double a, double b, double c) { return ::fma(a, b, c); }
   static __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 };
 
@@ -54,6 +56,8 @@ template <> struct M<float> {
   static __device__ __forceinline__ float floor(float x) { return ::floorf(x); }
   static __device__ __forceinline__ float fabs(float x) { return ::fabsf(x); }
   static __device__ __forceinline__ float fmod(float x, float y) { return ::fmodf(x, y); }
+  static __device__ __forceinline__ float trunc(float x) { return ::truncf(x); }
+  static __device__ __forceinline__ float fma(float a, float b, float c) { return ::fmaf(a, b, c); }
   static __device__ __forceinline__ bool finite(float x) { return isfinite(x); }
 };
 
