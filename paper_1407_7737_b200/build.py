@@ -16,7 +16,8 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
 LIB = HERE / "librobench_b200.so"
-SOURCES = [HERE / "csrc" / n for n in ("rb_capi.cu", "rb_kern_f64.cu", "rb_kern_f32.cu")]
+SOURCES = [HERE / "csrc" / n for n in ("rb_capi.cu", "rb_kern_f64.cu", "rb_kern_f32.cu",
+                                       "rb_kern_f64x.cu", "rb_kern_f32x.cu")]
 DEPS = SOURCES + sorted((HERE / "csrc").glob("*.cuh")) + [ROOT / "include" / "robench_b200.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

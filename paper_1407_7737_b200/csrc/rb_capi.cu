@@ -10,11 +10,19 @@
 #include <string>
 #include <vector>
 
-#include "rb_device.cuh"
+#include <map>
+
+#include "rb_fnspec.cuh"
 
 namespace rb {
 extern const void* const kernels_f64[N_VARIANTS];
 extern const void* const kernels_f32[N_VARIANTS];
+extern const void* const kernels_spec_f64[FN_COUNT_SPEC];
+extern const void* const kernels_spec_f32[FN_COUNT_SPEC];
+cudaError_t set_weier_f64x(const double* a_then_c);
+cudaError_t set_weier_f32x(const float* a_then_c);
+void phase_read_f64x(unsigned long long out[8], bool reset);
+void phase_read_f32x(unsigned long long out[8], bool reset);
 cudaError_t set_weier_f64(const double* a_then_c);
 cudaError_t set_weier_f32(const float* a_then_c);
 void phase_read_f64(unsigned long long out[8], bool reset);
@@ -75,6 +83,12 @@ struct Launch {
 int prefetch_mode() {
   const char* v = std::getenv("RB_PREFETCH");
   return v ? std::atoi(v) : -1;
+}
+
+// RB_SPEC=0 keeps hybrids / compositions on the generic kernel.
+int spec_mode() {
+  const char* v = std::getenv("RB_SPEC");
+  return v ? std::atoi(v) : 1;
 }
 
 // RB_L2PF=0 disables the L2 prefetch of upcoming X tiles (default on).
@@ -238,9 +252,9 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
   const int nf = pk->n_functions;
   e->exact_ok.assign(nf, 1);
   for (int pi = 0; pi < 2; ++pi) e->launch[pi].assign(nf, Launch());
-  std::vector<size_t> need[2] = {std::vector<size_t>(rb::N_VARIANTS, 0),
-                                 std::vector<size_t>(rb::N_VARIANTS, 0)};
+  std::map<const void*, size_t> need;       // dynamic shared memory per kernel
   std::vector<int> variant(nf, rb::N_VARIANTS - 1);
+  std::vector<int> spec(nf, -1);            // function-specialised kernel (rb_fnspec.cuh)
   for (int fi = 0; fi < nf; ++fi) {
     const rb_function& fn = pk->functions[fi];
     if (fn.category == RB_DISABLED) continue;
@@ -267,9 +281,23 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the DMMA unit table");
     if (fn.category == RB_BASIC && fn.n_members == 1 && first.n_segments == 1)
       variant[fi] = pk->segments[s0].kernel;
+    if (fi >= rb::FN_FIRST_SPEC && fi < rb::FN_FIRST_SPEC + rb::FN_COUNT_SPEC) {
+      // the pack's jobs must be exactly the compiled catalog's
+      const rb::JobList jl = rb::job_list(fi);
+      bool match = jl.n == s1 - s0;
+      for (int mi = 0, j = 0; match && mi < fn.n_members; ++mi) {
+        const rb_member& mm = pk->members[fn.member0 + mi];
+        for (int si = 0; si < mm.n_segments; ++si, ++j)
+          match = match && j < jl.n && jl.member[j] == mi &&
+                  jl.kernel[j] == pk->segments[mm.segment0 + si].kernel &&
+                  pk->segments[mm.segment0 + si].n_groups > 0;
+      }
+      if (match && spec_mode()) spec[fi] = fi - rb::FN_FIRST_SPEC;
+    }
     for (int pi = 0; pi < 2; ++pi) {
       Launch& L = e->launch[pi][fi];
       L.func = (pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[variant[fi]];
+      if (spec[fi] >= 0) L.func = (pi == 0 ? rb::kernels_spec_f64 : rb::kernels_spec_f32)[spec[fi]];
       L.max_q = std::max(max_q, 1);
       L.ldv = ldv;
       L.opt_rows = fn.category == RB_COMPOSITION ? fn.n_members : 0;
@@ -279,14 +307,11 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       if ((int)L.smem_nbuf[1] > optin)
         return fail(RB_E_UNSUPPORTED, "dimension too large for the shared-memory tile");
       const size_t top = (int)L.smem_nbuf[2] <= optin ? L.smem_nbuf[2] : L.smem_nbuf[1];
-      need[pi][variant[fi]] = std::max(need[pi][variant[fi]], top);
+      need[L.func] = std::max(need[L.func], top);
     }
   }
-  for (int pi = 0; pi < 2; ++pi)
-    for (int v = 0; v < rb::N_VARIANTS; ++v)
-      if (need[pi][v])
-        RB_CUDA(cudaFuncSetAttribute((pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[v],
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need[pi][v]));
+  for (const auto& kv : need)
+    RB_CUDA(cudaFuncSetAttribute(kv.first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.second));
   for (int fi = 0; fi < nf; ++fi) {
     if (pk->functions[fi].category == RB_DISABLED) continue;
     for (int pi = 0; pi < 2; ++pi) {
@@ -329,6 +354,8 @@ rb_status upload_series_constants(const rb_pack* pk) {
   if (found < 0) return RB_OK;
   RB_CUDA(rb::set_weier_f64(pk->values_f64 + found));
   RB_CUDA(rb::set_weier_f32(pk->values_f32 + found));
+  RB_CUDA(rb::set_weier_f64x(pk->values_f64 + found));
+  RB_CUDA(rb::set_weier_f32x(pk->values_f32 + found));
   return RB_OK;
 }
 
@@ -347,10 +374,15 @@ int64_t rb_launch_count(void) { return g_launches.load(); }
  * [load, stage, kernel, tile, tiles] summed over CTAs; zeros unless the
  * library was built with -DRB_PHASE_TIMING (tools/phase_timing.py). */
 void rb_debug_phases(int32_t precision, uint64_t out[8], int32_t reset) {
-  unsigned long long v[8];
-  if (precision == 0) rb::phase_read_f64(v, reset != 0);
-  else rb::phase_read_f32(v, reset != 0);
-  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  unsigned long long v[8], w[8];
+  if (precision == 0) {
+    rb::phase_read_f64(v, reset != 0);
+    rb::phase_read_f64x(w, reset != 0);
+  } else {
+    rb::phase_read_f32(v, reset != 0);
+    rb::phase_read_f32x(w, reset != 0);
+  }
+  for (int i = 0; i < 8; ++i) out[i] = v[i] + w[i];
 }
 
 void rb_struct_sizes(int64_t out[5]) {

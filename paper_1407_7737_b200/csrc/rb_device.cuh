@@ -727,6 +727,12 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
   return total;
 }
 
+// Function-specialised hybrids / compositions (rb_fnspec.cuh), kernel ids
+// SPEC_BASE + fid.
+constexpr int SPEC_BASE = 100;
+template <class T, int FID>
+__device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid);
+
 // Resident CTAs per SM the register budget is sized for.
 template <class T, int KID>
 constexpr int min_blocks() {
@@ -813,7 +819,9 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     RB_PHASE_MARK(c_loaded);
     RB_PHASE_ADD(0, c_loaded - c_tile);
     T result;
-    if constexpr (KID >= 0) {
+    if constexpr (KID >= SPEC_BASE) {
+      result = spec_value<T, KID - SPEC_BASE>(a, st, t, valid);
+    } else if constexpr (KID >= 0) {
       result = member_value<T, KID>(a, st, P.mem[0], t);
     } else if (P.fn.category != RB_COMPOSITION) {
       result = member_value<T, GENERIC>(a, st, P.mem[0], t);
