@@ -498,23 +498,35 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, co
       const int r0 = rq * 4 + pass * RR;
       if (r0 >= m) break;
       const float* B = a.values + G.mat + r0;
+      // column q: V row vq + q (4 points, one float4) and B row q (RR rows)
+      const float4* Vq = reinterpret_cast<const float4*>(s.VS + vq * TP + pq * 4);
+      constexpr int vstride = TP / 4;
+      const int bstride = m4;
+      int qb[10];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) qb[k] = G.qb[k];
       float t0[4][RR], t1[4][RR], t2[4][RR], acc[4][RR];
+      auto load_b = [&](const float* bp, float (&bb)[RR]) {
+        if constexpr (RR == 4) {
+          const float4 b = __ldg(reinterpret_cast<const float4*>(bp));
+          bb[0] = b.x; bb[1] = b.y; bb[2] = b.z; bb[3] = b.w;
+        } else {
+          const float2 b = __ldg(reinterpret_cast<const float2*>(bp));
+          bb[0] = b.x; bb[1] = b.y;
+        }
+      };
+      const float* bp = B;                       // B row q, advanced with q
 #pragma unroll
       for (int sl = 0; sl < 8; ++sl) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < RR; ++j) acc[i][j] = 0.0f;
-        for (int q = G.qb[sl]; q < G.qb[sl + 1]; ++q) {
-          const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
+#pragma unroll 2
+        for (int q = qb[sl]; q < qb[sl + 1]; ++q, bp += bstride) {
+          const float4 v = Vq[q * vstride];
           float bb[RR];
-          if constexpr (RR == 4) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(B + q * m4));
-            bb[0] = b.x; bb[1] = b.y; bb[2] = b.z; bb[3] = b.w;
-          } else {
-            const float2 b = __ldg(reinterpret_cast<const float2*>(B + q * m4));
-            bb[0] = b.x; bb[1] = b.y;
-          }
+          load_b(bp, bb);
           const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -541,15 +553,15 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, co
             }
           }
       }
-      for (int q = G.qb[8]; q < G.qb[9]; ++q) {
-        const float4 v = *reinterpret_cast<const float4*>(s.VS + (vq + q) * TP + pq * 4);
+      for (int q = qb[8]; q < qb[9]; ++q, bp += bstride) {
+        const float4 v = Vq[q * vstride];
         const float vv[4] = {v.x, v.y, v.z, v.w};
+        float bb[RR];
+        load_b(bp, bb);
 #pragma unroll
-        for (int j = 0; j < RR; ++j) {
-          const float b = __ldg(B + q * m4 + j);
+        for (int j = 0; j < RR; ++j)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], b));
-        }
+          for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], bb[j]));
       }
 #pragma unroll
       for (int j = 0; j < RR; ++j) {
