@@ -368,6 +368,27 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
 // n-tiles sharing (group, m-tile), so one A fragment per k-step feeds the
 // run.  Fragment layouts (PTX m16n8k4 .f64): a_i = (gid + 8i, tig),
 // b = (tig, gid), c_i = (gid + 8*(i>>1), 2*tig + (i&1)).
+// R (1 or 2) n-tiles of one (group, m-tile) over all k-steps: A = x - o
+// gathered through the column table, B pre-swizzled from the pack.
+template <int R>
+__device__ __forceinline__ void dmma_run(const double* X0, const double* X1, const int* qs,
+                                         const double* qo, const double* F, int nks,
+                                         double (&acc)[2][4]) {
+#pragma unroll 3
+  for (int ks = 0; ks < nks; ++ks) {
+    const int col = qs[ks * 4];
+    const double o = qo[ks * 4];
+    const double a0 = X0[col] - o;
+    const double a1 = X1[col] - o;
+    const double b0 = __ldg(F + ks * 32);
+    dmma_16x8x4(acc[0], a0, a1, b0);
+    if constexpr (R == 2) {
+      const double b1 = __ldg(F + (nks + ks) * 32);
+      dmma_16x8x4(acc[1], a0, a1, b1);
+    }
+  }
+}
+
 template <int NW, bool CHECK>
 __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int si,
                                       int warp) {
@@ -383,58 +404,43 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
     const int g = ud & 0xff, mt = (ud >> 8) & 0xff, nt0 = ud >> 16;
     const rb_group& G = P.grp[g];
     const int m = G.m, ntn = (m + 7) >> 3, nks = (m + 3) >> 2;
-    const int run = min(min(NTC, ntn - nt0), end - u);
+    const int run = min(min(2, ntn - nt0), end - u);
     const double* F = a.values + G.frag + (size_t)nt0 * nks * 32 + lane;
     const int* qs = s.qsrc + P.gq0[g] + tig;    // padded columns read x[.][0] * B = 0
     const double* qo = s.qo + P.gq0[g] + tig;
     const double* X0 = s.XS + (mt * 16 + gid) * a.dim;
     const double* X1 = X0 + 8 * a.dim;
-    double acc[NTC][4];
-#pragma unroll
-    for (int c = 0; c < NTC; ++c)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[c][i] = 0.0;
-    // k-steps in batches of KB: the batch's gathers and B loads issue before
-    // its DMMAs, so one load latency is paid per batch, not per k-step
-    for (int k0 = 0; k0 < nks; k0 += KB) {
-      double fa0[KB], fa1[KB], fb[KB][NTC];
-#pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        if (k0 + k < nks) {
-          const int col = qs[(k0 + k) * 4];
-          const double o = qo[(k0 + k) * 4];
-          fa0[k] = X0[col] - o;
-          fa1[k] = X1[col] - o;
-#pragma unroll
-          for (int c = 0; c < NTC; ++c)
-            if (c < run) fb[k][c] = __ldg(F + (c * nks + k0 + k) * 32);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < KB; ++k)
-        if (k0 + k < nks) {
-#pragma unroll
-          for (int c = 0; c < NTC; ++c)
-            if (c < run) dmma_16x8x4(acc[c], fa0[k], fa1[k], fb[k][c]);
-        }
-    }
+    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    // the run length is warp-uniform: unpredicated mma.sync in both loops
+    if (run == 2) dmma_run<2>(X0, X1, qs, qo, F, nks, acc);
+    else dmma_run<1>(X0, X1, qs, qo, F, nks, acc);
+    // epilogue: z = acc - cz, scattered to the rows' z positions; rows come
+    // in pairs (2 tig, 2 tig + 1), so the tables are read as pairs
     const int* prow = s.prow + P.gq0[g];
     const double* cz = s.cz + P.gq0[g];
     const int p0 = mt * 16 + gid;
+    double* Z0 = s.ZS + p0 * a.ldz;
+    double* Z1 = Z0 + 8 * a.ldz;
     uint32_t e0 = 0u, e1 = 0u;                  // max exponent field per point
 #pragma unroll
-    for (int c = 0; c < NTC; ++c) {
-      if (c >= run) break;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int rr = (nt0 + c) * 8 + 2 * tig + (i & 1);
-        if (rr < m) {
-          const double zv = acc[c][i] - cz[rr];
-          s.ZS[(p0 + ((i >> 1) << 3)) * a.ldz + prow[rr]] = zv;
-          if (CHECK) {
-            const uint32_t e = (uint32_t)__double2hiint(zv) & 0x7ff00000u;
-            if (i < 2) e0 = max(e0, e); else e1 = max(e1, e);
-          }
+    for (int c = 0; c < 2; ++c) {
+      const int rr = (nt0 + c) * 8 + 2 * tig;
+      if (c < run && rr < m) {
+        const int2 pr = *reinterpret_cast<const int2*>(prow + rr);
+        const double2 cc = *reinterpret_cast<const double2*>(cz + rr);
+        const double z00 = acc[c][0] - cc.x, z10 = acc[c][2] - cc.x;
+        Z0[pr.x] = z00;
+        Z1[pr.x] = z10;
+        double z01 = 0.0, z11 = 0.0;
+        if (rr + 1 < m) {
+          z01 = acc[c][1] - cc.y;
+          z11 = acc[c][3] - cc.y;
+          Z0[pr.y] = z01;
+          Z1[pr.y] = z11;
+        }
+        if (CHECK) {
+          e0 = max(e0, max((uint32_t)__double2hiint(z00), (uint32_t)__double2hiint(z01)) & 0x7ff00000u);
+          e1 = max(e1, max((uint32_t)__double2hiint(z10), (uint32_t)__double2hiint(z11)) & 0x7ff00000u);
         }
       }
     }
