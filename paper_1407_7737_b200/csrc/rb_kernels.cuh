@@ -95,7 +95,9 @@ template <class T> __device__ __forceinline__ T katsuura_row(T zj) {
   for (int i = 0; i < 32; ++i) {
     const T p2 = T(1ull << (i + 1));  // 2**(i+1), exact
     const T w = p2 * zj;
-    r[i & 7] = r[i & 7] + M<T>::fabs(w - M<T>::floor(w + C<T>(0.5))) / p2;
+    // "/ 2**(i+1)" as a product with the exact reciprocal: both are the
+    // correctly rounded scaling of the same value (no division sequence)
+    r[i & 7] = r[i & 7] + M<T>::fabs(w - M<T>::floor(w + C<T>(0.5))) * T(1.0 / double(1ull << (i + 1)));
   }
   return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
 }
@@ -191,8 +193,13 @@ __device__ __forceinline__ T kernel_value_k(const Pt<T>& P) {
     acc = acc + __shfl_xor_sync(RB_FULL, acc, 4, 8);
     return acc - P.ctab[42];
   } else if constexpr (K == K_GRIEWANK) {                             // :109-112
+    // ctab: float32 np.sqrt(arange(1, d+1)) (divided by, as the reference);
+    // float64 its reciprocal (multiplied by, to tolerance) -- pack.py
+    const T* sq_i = P.ctab;
     const T s = pw8<T>(0, d, square, l8);
-    const T p = prod8<T>(d, [&](int i) { return M<T>::cos(z[i] / M<T>::sqrt(T(i + 1))); }, l8);
+    const T p = prod8<T>(d, [&](int i) {
+      return M<T>::cos(sizeof(T) == 8 ? z[i] * sq_i[i] : z[i] / sq_i[i]);
+    }, l8);
     return (s / C<T>(4000.0) - p) + C<T>(1.0);
   } else if constexpr (K == K_RASTRIGIN) {                            // :115-117
     return pw8<T>(0, d, [&](int i) {

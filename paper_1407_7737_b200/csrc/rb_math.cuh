@@ -66,7 +66,11 @@ template <> struct M<float> {
 // (rb_svml_powf.cuh).  Scalar powers (np.float32 ** float) go through libm
 // powf in NumPy and use M<T>::pow here.
 template <class T> __device__ __forceinline__ T apow(T a, T b);
-template <> __device__ __forceinline__ double apow<double>(double a, double b) { return ::pow(a, b); }
+// float64 to tolerance: exp(b log a) (|b log a| <= ~20 on the paths that use
+// it: powers, SchaffersF7 -> relative error ~1e-15), a = 0 -> 0 for b > 0
+template <> __device__ __forceinline__ double apow<double>(double a, double b) {
+  return ::exp(b * ::log(a));
+}
 template <> __device__ __forceinline__ float apow<float>(float a, float b) { return rb_svml::powf_np(a, b); }
 
 // Python-double constant as NumPy casts it into the working dtype (NEP 50:

@@ -69,6 +69,11 @@ def kernel_constants(kernel: str, d: int, dt) -> np.ndarray:
         arg = 2.0 * np.pi * bk        # left operand of "* (z[:, None] + 0.5)"
         base = np.sum(ak * np.cos(np.pi * bk))
         return np.concatenate([ak, arg, np.asarray([d * base], dtype=dt)]).astype(dt)
+    if kernel == "griewank":                                   # kernels.py:111-112
+        root = np.sqrt(np.arange(1, d + 1, dtype=dt))
+        # float32 divides by NumPy's sqrt like the reference; float64
+        # multiplies by the reciprocal (parity to tolerance)
+        return root if dt == np.float32 else 1.0 / root
     if kernel == "katsuura":                                   # kernels.py:183-184
         return np.asarray([10.0 / d**1.2, 10.0 / (d * d)], dtype=dt)
     return np.zeros(0, dtype=dt)
