@@ -60,11 +60,14 @@ typedef struct rb_group {
   int32_t row;      /* index[row + r]: output position (into z) of block row r */
   int32_t mat;      /* values[mat + q*m4 + r] = block[r][column of q], m4 = m rounded up to 4
                        (rows zero-padded; float32 exact-order rotate, 16-byte aligned) */
-  int32_t frag;     /* values_f64[frag + ((nt*nks + ks)*32 + lane)] = scale * mat[4ks + lane%4][8nt + lane/4]
-                       (zero outside m x m): the mma.m16n8k4 B fragments of the segment's
-                       scaled block, nt < ceil(m/8), ks < ceil(m/4) (float64 DMMA rotate) */
+  int32_t frag;     /* values_f64[frag + ((nt*nks + ks)*32 + lane)] = scale * block[8nt + lane/4][c(4ks + lane%4)]
+                       (zero outside m x m), c(q) the q-th column in col64 order: the
+                       mma.m16n8k4 B fragments of the segment's scaled block, nt < ceil(m/8),
+                       ks < ceil(m/4) (float64 DMMA rotate) */
   int32_t cz;       /* values_f64[cz + r] = -pre * sum_q mat[q][r] - post: the float64 rotate
                        computes z_r = sum_q (scale B)[q][r] (x[src_q] - o[src_q]) - cz[r] */
+  int32_t col64;    /* index[col64 + q]: input position of the q-th float64 column (an order
+                       whose 4-column k-steps read shared memory without bank conflicts) */
 } rb_group;
 
 /* One kernel application: v = scale*((x - o)[src..]) + pre; z = R v + post;

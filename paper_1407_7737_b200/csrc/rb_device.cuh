@@ -248,7 +248,7 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
       for (int gi = 0; gi < seg.n_groups; ++gi) {
         const int g = seg.group0 - P.grp_base + gi;
         const rb_group& G = P.grp[g];
-        const int32_t* cols = a.index + G.col;
+        const int32_t* cols = a.index + (sizeof(T) == 8 ? G.col64 : G.col);
         const int32_t* rows = a.index + G.row;
         for (int q = threadIdx.x; q < round8(G.m); q += nth) {
           int src = 0, row = 0;

@@ -30,7 +30,8 @@ import numpy as np
 from . import catalog, instances
 
 GROUP_DT = np.dtype([("m", "<i4"), ("qb", "<i4", (10,)), ("col", "<i4"),
-                     ("row", "<i4"), ("mat", "<i4"), ("frag", "<i4"), ("cz", "<i4")])
+                     ("row", "<i4"), ("mat", "<i4"), ("frag", "<i4"), ("cz", "<i4"),
+                     ("col64", "<i4")])
 SEGMENT_DT = np.dtype({
     "names": ["kernel", "d", "src", "n_groups", "group0", "ctab", "scale", "pre", "post"],
     "formats": ["<i4"] * 6 + ["<f8"] * 3,
@@ -79,6 +80,36 @@ def kernel_constants(kernel: str, d: int, dt) -> np.ndarray:
     return np.zeros(0, dtype=dt)
 
 
+def fp64_column_order(x_col, dim: int) -> list[int]:
+    """Order of a block's columns for the float64 DMMA A fragments: each
+    k-step gathers 4 columns for 8 points whose X rows are ``dim`` doubles
+    apart; a half-warp (4 points x 4 columns) reads shared memory without
+    bank conflicts when the 16 double-banks (row_offset + column) mod 16
+    are distinct.  Greedy: fill every k-step with mutually conflict-free
+    columns first."""
+    offs = [(g * dim) % 16 for g in range(4)]
+    banks = [frozenset((o + int(c)) % 16 for o in offs) for c in x_col]
+    rem = list(range(len(x_col)))
+    order: list[int] = []
+    while rem:
+        used: set = set()
+        pick: list[int] = []
+        for k in rem:
+            if not (banks[k] & used):
+                pick.append(k)
+                used |= banks[k]
+                if len(pick) == 4:
+                    break
+        for k in rem:                     # no conflict-free 4th column: take any
+            if len(pick) == 4:
+                break
+            if k not in pick:
+                pick.append(k)
+        order += pick
+        rem = [k for k in rem if k not in pick]
+    return order
+
+
 class _Builder:
     def __init__(self, dim: int):
         self.dim = dim
@@ -92,6 +123,7 @@ class _Builder:
         self.max_exact_len = 0   # longest rotated segment (exact-order fp32 bound)
         self.max_q = 0           # widest per-segment sum of 4-padded group sizes
         self.max_d = 0
+        self.group_src: list = []   # (block, segment positions, scale) per group
 
     # -- tables
     def values(self, a64, a32=None) -> int:
@@ -138,21 +170,35 @@ class _Builder:
         m4, nt, nk = (m + 3) // 4 * 4, (m + 7) // 8, (m + 3) // 4
         padded = np.zeros((nk * 4, nt * 8))
         padded[:m, :m] = mat
-        lane = np.arange(32)
-        # frag[nt][ks][lane] = padded[4ks + lane%4, 8nt + lane/4]
-        frag = padded[(4 * np.arange(nk)[None, :, None] + lane % 4)[..., :],
-                      (8 * np.arange(nt)[:, None, None] + lane // 4)]
         rec = np.zeros((), dtype=GROUP_DT)
         rec["m"] = m
         rec["qb"] = qb
         rec["col"] = self.ints([cols[k] for k in order])
         rec["row"] = self.ints(rows)
         rec["mat"] = self.values(padded[:m, :m4])
-        rec["frag"] = self.values(scale * frag, frag.astype(np.float32))
         cz = -np.longdouble(pre) * mat.astype(np.longdouble).sum(axis=0) - np.longdouble(post)
         rec["cz"] = self.values(cz.astype(np.float64))
+        rec["frag"] = rec["col64"] = -1                  # member(): needs the x columns
         self.groups.append(rec)
+        self.group_src.append((block, cols, scale))
         return len(self.groups) - 1
+
+    def fp64_layout(self, gi: int, x_col) -> None:
+        """float64 DMMA operands of group gi: its own column order (the
+        float64 sum order is free) and the B fragments in that order.
+        ``x_col[k]``: X column feeding block column k."""
+        block, cols, scale = self.group_src[gi]
+        order = fp64_column_order(x_col, self.dim)
+        m = block.shape[0]
+        nt, nk = (m + 7) // 8, (m + 3) // 4
+        padded = np.zeros((nk * 4, nt * 8))
+        padded[:m, :m] = block[:, order].T                     # [q, r] = block[r, order[q]]
+        lane = np.arange(32)
+        # frag[nt][ks][lane] = padded[4ks + lane%4, 8nt + lane/4]
+        frag = padded[(4 * np.arange(nk)[None, :, None] + lane % 4)[..., :],
+                      (8 * np.arange(nt)[:, None, None] + lane // 4)]
+        self.groups[gi]["frag"] = self.values(scale * frag, frag.astype(np.float32))
+        self.groups[gi]["col64"] = self.ints([cols[k] for k in order])
 
     def segment(self, kernel: str, d: int, src: int, blocks) -> int:
         """blocks: list of (block, cols, rows) or [] when not rotated."""
@@ -177,6 +223,11 @@ class _Builder:
         return len(self.segments) - 1
 
     def member(self, shift, segs: list[int], perm=None, sigma=0.0, height=0.0, bias=0.0) -> int:
+        for si in segs:
+            seg = self.segments[si]
+            for gi in range(int(seg["group0"]), int(seg["group0"]) + int(seg["n_groups"])):
+                pos = np.asarray(self.group_src[gi][1], dtype=np.int64) + int(seg["src"])
+                self.fp64_layout(gi, np.asarray(perm)[pos] if perm is not None else pos)
         rec = np.zeros((), dtype=MEMBER_DT)
         rec["n_segments"] = len(segs)
         rec["segment0"] = segs[0]

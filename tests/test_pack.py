@@ -107,12 +107,16 @@ def test_dmma_fragments_match_q_ordered_block():
         m = int(g["m"])
         nt, nk, m4 = (m + 7) // 8, (m + 3) // 4, (m + 3) // 4 * 4
         mat = pk.values_f64[g["mat"]:g["mat"] + m * m4].reshape(m, m4)
+        col = pk.index[g["col"]:g["col"] + m]
+        col64 = pk.index[g["col64"]:g["col64"] + m]
+        assert sorted(col) == sorted(col64)
+        qpos = {int(c): q for q, c in enumerate(col)}           # q-order row of mat per column
         frag = pk.values_f64[g["frag"]:g["frag"] + nt * nk * 32].reshape(nt, nk, 32)
         for a in range(nt):
             for ks in range(nk):
                 for lane in range(32):
                     q, r = 4 * ks + lane % 4, 8 * a + lane // 4
-                    want = scale * mat[q, r] if (q < m and r < m) else 0.0
+                    want = scale * mat[qpos[int(col64[q])], r] if (q < m and r < m) else 0.0
                     assert frag[a, ks, lane] == want
         assert g["mat"] % 4 == 0 and g["frag"] % 4 == 0
 
@@ -141,9 +145,24 @@ def test_fp64_offsets_restate_the_transform(dim):
                 want = mat.T @ v + seg["post"]
                 cz = pk.values_f64[g["cz"]:g["cz"] + m]
                 got = (seg["scale"] * mat).T @ (x[src] - o[src]) - cz
+                # the float64 column order feeds the same columns
+                pos64 = pk.index[g["col64"]:g["col64"] + m] + seg["src"]
+                assert sorted(pos64) == sorted(pos)
                 assert np.allclose(got, want, rtol=1e-12, atol=1e-10 * max(1.0, np.abs(want).max()))
                 if seg["pre"] == 0.0:
                     assert np.all(-cz == seg["post"])
+
+
+def test_fp64_column_order_avoids_bank_conflicts():
+    # D=100: X rows are 100 doubles apart (4 mod 16 banks): a k-step is
+    # conflict-free iff its 4 columns differ mod 4; the greedy order achieves
+    # it wherever the residue counts allow
+    cols = list(range(0, 100, 3))[:34]
+    order = P.fp64_column_order(cols, 100)
+    assert sorted(order) == list(range(34))
+    full = [order[i:i + 4] for i in range(0, 32, 4)]
+    good = sum(len({cols[k] % 4 for k in ks}) == 4 for ks in full)
+    assert good >= 6
 
 
 def test_kernel_constants_follow_numpy():
