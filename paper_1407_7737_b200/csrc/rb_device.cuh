@@ -669,41 +669,87 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
 // lane's point (row x of the X tile) from its squared distances to every
 // member optimum: one-hot on an optimum (d2 < 1e-24), uniform if all
 // weights underflow.
-template <class T>
+// NM > 0: member count known at compile time (function-specialised kernels).
+template <class T, int NM = 0>
 __device__ __forceinline__ void composition_weights(const Args<T>& a, const PlanHead& P, const T* x,
                                                     const T* opt, int l8, T (&om)[MAX_MEMBERS]) {
-  const int nm = P.fn.n_members;
+  const int nm = NM > 0 ? NM : P.fn.n_members;
+  const int dim = a.dim;
   T d2[MAX_MEMBERS];
 #pragma unroll
   for (int k = 0; k < MAX_MEMBERS; ++k) {
     d2[k] = T(0);
     om[k] = T(0);
-    if (k < nm) {
-      const T* o = opt + k * a.dim;
-      d2[k] = pw8<T>(0, a.dim, [&](int j) { const T u = x[j] - o[j]; return u * u; }, l8);
+  }
+  if (dim <= 128) {
+    // every member's sum((x - o)**2) in one pass over x (5 independent
+    // chains per lane), in pw8's single-leaf order: lane k takes j = k (mod 8)
+    // below the last multiple of 8, xor butterfly, then the tail in order
+    const int main_len = (sizeof(T) == 8 || dim < 8) ? (sizeof(T) == 8 ? dim : 0) : dim - (dim & 7);
+    T r[MAX_MEMBERS];
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k) r[k] = T(0);
+    for (int j = l8; j < main_len; j += 8) {
+      const T xj = x[j];
+#pragma unroll
+      for (int k = 0; k < MAX_MEMBERS; ++k)
+        if (k < nm) {
+          const T u = xj - opt[k * dim + j];
+          r[k] = r[k] + u * u;
+        }
     }
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k) {
+      if (main_len) {
+        r[k] = r[k] + __shfl_xor_sync(RB_FULL, r[k], 1, 8);
+        r[k] = r[k] + __shfl_xor_sync(RB_FULL, r[k], 2, 8);
+        r[k] = r[k] + __shfl_xor_sync(RB_FULL, r[k], 4, 8);
+      }
+      const int tail = dim - main_len;
+      if (tail) {
+        T v = T(0);
+        if (k < nm && l8 < tail) {
+          const T u = x[main_len + l8] - opt[k * dim + main_len + l8];
+          v = u * u;
+        }
+        for (int q = 0; q < tail; ++q) r[k] = r[k] + __shfl_sync(RB_FULL, v, q, 8);
+      }
+      d2[k] = k < nm ? r[k] : T(0);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < MAX_MEMBERS; ++k)
+      if (k < nm) {
+        const T* o = opt + k * dim;
+        d2[k] = pw8<T>(0, dim, [&](int j) { const T u = x[j] - o[j]; return u * u; }, l8);
+      }
   }
   T mn = d2[0];
   int am = 0;
 #pragma unroll
   for (int k = 1; k < MAX_MEMBERS; ++k)
     if (k < nm && d2[k] < mn) { mn = d2[k]; am = k; }
+  // lane k of the point computes member k's Gaussian weight, then all lanes
+  // gather them (the 8 lanes would otherwise repeat 5 pow/exp each); done
+  // before the branch below: the points of a warp may take different ones
+  T dk = d2[0], sgk = (T)P.mem[0].sigma;
+#pragma unroll
+  for (int k = 1; k < MAX_MEMBERS; ++k)
+    if (l8 == k && k < nm) { dk = d2[k]; sgk = (T)P.mem[k].sigma; }
+  // d2 ** -0.5: float64 to tolerance via rsqrt; float32 NumPy's SVML powf
+  const T ih = sizeof(T) == 8 ? (T)::rsqrt((double)dk) : apow<T>(dk, C<T>(-0.5));
+  const T wk = ih * M<T>::exp(-dk / (C<T>(2.0 * dim) * (sgk * sgk)));
+  T w[MAX_MEMBERS];
+#pragma unroll
+  for (int k = 0; k < MAX_MEMBERS; ++k) w[k] = __shfl_sync(RB_FULL, wk, k, 8);
   if (mn < C<T>(1.0000000000000002e-24)) {          // 1e-12**2: on an optimum
 #pragma unroll
     for (int k = 0; k < MAX_MEMBERS; ++k) om[k] = (k == am) ? T(1) : T(0);
   } else {
-    T w[MAX_MEMBERS], tot = T(0);
+    T tot = T(0);
 #pragma unroll
-    for (int k = 0; k < MAX_MEMBERS; ++k) {
-      w[k] = T(0);
-      if (k < nm) {
-        const T sg = (T)P.mem[k].sigma;
-        // d2 ** -0.5: float64 to tolerance via rsqrt; float32 NumPy's SVML powf
-        const T ih = sizeof(T) == 8 ? (T)::rsqrt((double)d2[k]) : apow<T>(d2[k], C<T>(-0.5));
-        w[k] = ih * M<T>::exp(-d2[k] / (C<T>(2.0 * a.dim) * (sg * sg)));
-        tot = tot + w[k];
-      }
-    }
+    for (int k = 0; k < MAX_MEMBERS; ++k)
+      if (k < nm) tot = tot + w[k];
 #pragma unroll
     for (int k = 0; k < MAX_MEMBERS; ++k)
       if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;

@@ -88,8 +88,9 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
   T om[MAX_MEMBERS];
 #pragma unroll
   for (int k = 0; k < MAX_MEMBERS; ++k) om[k] = T(0);
+  RB_PHASE_MARK(cw0);
   if constexpr (comp) {
-    composition_weights<T>(a, P, s.XS + p * a.dim, s.opt, l8, om);
+    composition_weights<T, L.member[L.n - 1] + 1>(a, P, s.XS + p * a.dim, s.opt, l8, om);
     const int nm = P.fn.n_members;
     if (l8 == 0 && valid) {
 #pragma unroll
@@ -98,6 +99,8 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
     }
     __syncthreads();
   }
+  RB_PHASE_MARK(cw1);
+  RB_PHASE_ADD(5, cw1 - cw0);
   T g = T(0), total = T(0);
 #pragma unroll 1
   for (int j = 0; j < L.n; ++j) {
@@ -108,10 +111,15 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
     if (comp && t.live == 0u) continue;
     const rb_member& mem = P.mem[mi];
     const rb_segment& seg = P.seg[P.job_seg[j]];
+    RB_PHASE_MARK(c0);
     const T* zb = stage_segment(a, s, mem, seg, t);
+    RB_PHASE_MARK(c1);
     const Pt<T> pt{zb + p * a.ldz, seg.d, l8, a.values + seg.ctab};
     const T v = spec_kernel<T, FID, 0>(j, pt);
     __syncthreads();                               // z is rewritten by the next job
+    RB_PHASE_MARK(c2);
+    RB_PHASE_ADD(1, c1 - c0);
+    RB_PHASE_ADD(2, c2 - c1);
     g = first ? v : g + v;
     if (last) {
       if (comp) {

@@ -25,9 +25,9 @@ for prec in precs:
         torch.cuda.synchronize()
         ph = _lib.debug_phases(prec, reset=True)
         tiles = max(ph[4], 1)
-        load, stage, kern, tot = (ph[i] / tiles for i in range(4))
-        other = tot - load - stage - kern
+        load, stage, kern, tot, _, wts = (ph[i] / tiles for i in range(6))
+        other = tot - load - stage - kern - wts
         print(f"fn {fn:2d} {prec:6s} clk/tile/CTA {tot:8.0f}: load {load:7.0f} ({100*load/tot:4.1f}%)  "
               f"z-stage {stage:7.0f} ({100*stage/tot:4.1f}%)  kernel {kern:7.0f} ({100*kern/tot:4.1f}%)  "
-              f"other {other:7.0f} ({100*other/tot:4.1f}%)")
+              f"weights {wts:7.0f} ({100*wts/tot:4.1f}%)  other {other:7.0f} ({100*other/tot:4.1f}%)")
 eng.dispose()
