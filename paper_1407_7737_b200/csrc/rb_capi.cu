@@ -266,16 +266,19 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
     if (fn.n_members > rb::MAX_MEMBERS || s1 - s0 > rb::MAX_SEGMENTS || g1 - g0 > rb::MAX_GROUPS)
       return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the plan limits");
     int max_q = 0, ldv = 4, units = 0;
-    for (int si = s0; si < s1; ++si) {
-      const rb_segment& sg = pk->segments[si];
+    for (int mi = 0; mi < fn.n_members; ++mi) {    // fp32 V rows: a member's chunks at once
+      const rb_member& mm = pk->members[fn.member0 + mi];
       int q4 = 0;
-      for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
-        max_q += rb::round8(pk->groups[g].m);
-        q4 += (pk->groups[g].m + 3) & ~3;
-        units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
+      for (int si = mm.segment0; si < mm.segment0 + mm.n_segments; ++si) {
+        const rb_segment& sg = pk->segments[si];
+        for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
+          max_q += rb::round8(pk->groups[g].m);
+          q4 += (pk->groups[g].m + 3) & ~3;
+          units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
+        }
+        if (sg.n_groups && sg.d > 128) e->exact_ok[fi] = 0;
       }
       ldv = std::max(ldv, q4);
-      if (sg.n_groups && sg.d > 128) e->exact_ok[fi] = 0;
     }
     if (units > rb::MAX_UNITS)
       return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the DMMA unit table");

@@ -98,6 +98,7 @@ struct PlanHead {
   rb_segment seg[MAX_SEGMENTS];
   rb_group grp[MAX_GROUPS];
   int gq0[MAX_GROUPS];            // group g's slice of the per-column tables (8-aligned)
+  int8_t grp_seg[MAX_GROUPS];     // plan segment owning group g
   unsigned long long mbar[2];     // TMA completion barriers, one per X buffer
   uint32_t live;                  // valid points of the current tile
   uint32_t livek[MAX_MEMBERS];    // compositions: valid points with a nonzero weight, per member
@@ -230,6 +231,7 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
     for (int si = 0; si < P.n_seg; ++si) {
       P.unit_off[si] = nu;
       const int g0 = P.seg[si].group0 - P.grp_base;
+      for (int g = g0; g < g0 + P.seg[si].n_groups; ++g) P.grp_seg[g] = (int8_t)si;
       for (int g = g0; g < g0 + P.seg[si].n_groups; ++g)
         for (int mt = 0; mt < TP / 16; ++mt)
           for (int nt = 0; nt < (P.grp[g].m + 7) >> 3 && nu < MAX_UNITS; ++nt)
@@ -257,7 +259,7 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
             const int pos = cols[q];
             src = mem.perm >= 0 ? a.index[mem.perm + seg.src + pos] : pos;
             ov = o[src];
-            row = rows[q];
+            row = rows[q] + seg.src;       // chunk k's z at offset src_k (hybrid members)
             if (sizeof(T) == 8) cv = a.values[G.cz + q];     // indexed by block row q
           }
           s.qsrc[P.gq0[g] + q] = src;
@@ -390,13 +392,13 @@ __device__ __forceinline__ void dmma_run(const double* X0, const double* X1, con
 }
 
 template <int NW, bool CHECK>
-__device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int si,
-                                      int warp) {
+__device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int s_first,
+                                      int s_end, int warp) {
   const PlanHead& P = *s.P;
   const int lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int u0 = P.unit_off[si];
-  const int total = P.unit_off[si + 1] - u0;
+  const int u0 = P.unit_off[s_first];
+  const int total = P.unit_off[s_end] - u0;
   const int end = (warp + 1) * total / NW;
   uint32_t nf = 0u;
   for (int u = warp * total / NW; u < end;) {
@@ -451,9 +453,11 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
   return nf;
 }
 
+// z of plan segments [s_first, s_end) (the chunks of one member, side by side)
 template <bool CHECK>
-__device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, const rb_segment& seg) {
-  return rotate_f64<NWARPS, CHECK>(a, s, (int)(&seg - s.P->seg), threadIdx.x >> 5);
+__device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, int s_first,
+                                  int s_end) {
+  return rotate_f64<NWARPS, CHECK>(a, s, s_first, s_end, threadIdx.x >> 5);
 }
 
 // ------------------------------------------------------------ rotate fp32
@@ -461,14 +465,17 @@ __device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, 
 // accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
 // ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
 template <bool CHECK>
-__device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, const rb_segment& seg) {
+__device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, int s_first,
+                                  int s_end) {
   const PlanHead& P = *s.P;
-  const int g0 = seg.group0 - P.grp_base;
-  const float scale = (float)seg.scale, pre = (float)seg.pre, post = (float)seg.post;
+  const int g0 = P.seg[s_first].group0 - P.grp_base;
+  const int ng = P.seg[s_end - 1].group0 + P.seg[s_end - 1].n_groups - P.seg[s_first].group0;
   // gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre   (engine.py:97-100)
   {
     int vq = 0;
-    for (int g = 0; g < seg.n_groups; ++g) {
+    for (int g = 0; g < ng; ++g) {
+      const rb_segment& sg = P.seg[P.grp_seg[g0 + g]];
+      const float scale = (float)sg.scale, pre = (float)sg.pre;
       const int kp = round4(P.grp[g0 + g].m);
       const int* qs = s.qsrc + P.gq0[g0 + g];
       const float* qo = s.qo + P.gq0[g0 + g];
@@ -483,7 +490,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, co
   }
   __syncthreads();
   int total = 0;
-  for (int g = 0; g < seg.n_groups; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
+  for (int g = 0; g < ng; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
   uint32_t nf = 0u;
   for (int t = threadIdx.x; t < total; t += NT) {
     int g = g0, rem = t, vq = 0;
@@ -495,6 +502,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, co
       ++g;
     }
     const rb_group& G = P.grp[g];
+    const float post = (float)P.seg[P.grp_seg[g]].post;
     const int pq = rem % (TP / 4), rq = rem / (TP / 4);
     const int m = G.m, m4 = round4(m);
     const int* prow = s.prow + P.gq0[g];
@@ -610,14 +618,18 @@ __device__ void fetch_x(const Args<T>& a, const Smem<T>& s, TileCtx& t) {
   t.x_ready = true;
 }
 
-// ---------------------------------------------------------- one segment
-// z of one segment for all points of the tile, then barrier; returns where
-// z lives (row stride ldz).
+// ----------------------------------------------------------- one member
+// z of every segment of one member for all points of the tile, then one
+// barrier: the chunks of a hybrid member are rotated in the same pass and
+// their z laid side by side (chunk k at offset src_k, pack.py).  Returns
+// where z lives (row stride ldz).
 template <class T>
-__device__ const T* stage_segment(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
-                                  const rb_segment& seg, TileCtx& t) {
+__device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
+                                 TileCtx& t) {
+  const PlanHead& P = *s.P;
   uint32_t nf = 0u;
-  const T* zb = s.ZS;
+  const int s_first = mem.segment0 - P.seg_base, s_end = s_first + mem.n_segments;
+  const rb_segment& seg = P.seg[s_first];
   if (seg.n_groups == 0) {                 // shift-only ids 10 and 15 (engine.py:96-104)
     T* zw = s.ZS;
     const T* o = a.values + mem.shift;
@@ -633,35 +645,36 @@ __device__ const T* stage_segment(const Args<T>& a, const Smem<T>& s, const rb_m
       if (t.check_z && not_finite(v)) nf |= 1u << p;
     }
   } else {
-    nf = t.check_z ? rotate<true>(a, s, seg) : rotate<false>(a, s, seg);
+    nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
   }
   if (nf & t.live) atomicOr(a.flag, 2);
   __syncthreads();
-  return zb;
+  return s.ZS;
 }
 
 // Value of one member (basic function, hybrid, or composition member) for
-// the calling lane's point.
+// the calling lane's point: one staging pass, then the chunk kernels in
+// order (hybrid.py:105-115: 0 + K_0 + K_1 + ...).
 template <class T, int KID>
 __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, TileCtx& t) {
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
+  RB_PHASE_MARK(c0);
+  const T* zb = stage_member(a, s, mem, t);
+  RB_PHASE_MARK(c1);
   T total = T(0);
   for (int si = 0; si < mem.n_segments; ++si) {
     const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
-    RB_PHASE_MARK(c0);
-    const T* zb = stage_segment(a, s, mem, seg, t);
-    RB_PHASE_MARK(c1);
-    const Pt<T> pt{zb + p * a.ldz, seg.d, l8, a.values + seg.ctab};
+    const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab};
     T v;
     if constexpr (KID >= 0) v = kernel_value_k<T, KID>(pt);
     else v = kernel_value<T>(seg.kernel, pt);
-    total = (si == 0) ? v : total + v;   // hybrid.py:105-115: 0 + K_0 + K_1 + ...
-    __syncthreads();                      // z is rewritten by the next segment
-    RB_PHASE_MARK(c2);
-    RB_PHASE_ADD(1, c1 - c0);
-    RB_PHASE_ADD(2, c2 - c1);
+    total = (si == 0) ? v : total + v;
   }
+  __syncthreads();                      // z is rewritten by the next member / tile
+  RB_PHASE_MARK(c2);
+  RB_PHASE_ADD(1, c1 - c0);
+  RB_PHASE_ADD(2, c2 - c1);
   return total;
 }
 

@@ -101,37 +101,43 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
   }
   RB_PHASE_MARK(cw1);
   RB_PHASE_ADD(5, cw1 - cw0);
-  T g = T(0), total = T(0);
+  T total = T(0);
 #pragma unroll 1
-  for (int j = 0; j < L.n; ++j) {
-    const int mi = P.job_mem[j];
-    const bool first = j == 0 || P.job_mem[j - 1] != mi;
-    const bool last = j == L.n - 1 || P.job_mem[j + 1] != mi;
-    if (comp && first) t.live = P.livek[mi];
-    if (comp && t.live == 0u) continue;
+  for (int j0 = 0; j0 < L.n;) {
+    // member mi = jobs [j0, j1): one staging pass, then its chunk kernels
+    const int mi = P.job_mem[j0];
+    int j1 = j0 + 1;
+    while (j1 < L.n && P.job_mem[j1] == mi) ++j1;
+    if (comp) t.live = P.livek[mi];
+    if (comp && t.live == 0u) {                    // composition.py:163-164
+      j0 = j1;
+      continue;
+    }
     const rb_member& mem = P.mem[mi];
-    const rb_segment& seg = P.seg[P.job_seg[j]];
     RB_PHASE_MARK(c0);
-    const T* zb = stage_segment(a, s, mem, seg, t);
+    const T* zb = stage_member(a, s, mem, t);
     RB_PHASE_MARK(c1);
-    const Pt<T> pt{zb + p * a.ldz, seg.d, l8, a.values + seg.ctab};
-    const T v = spec_kernel<T, FID, 0>(j, pt);
-    __syncthreads();                               // z is rewritten by the next job
+    T g = T(0);
+    for (int j = j0; j < j1; ++j) {
+      const rb_segment& seg = P.seg[P.job_seg[j]];
+      const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab};
+      const T v = spec_kernel<T, FID, 0>(j, pt);
+      g = j == j0 ? v : g + v;                     // hybrid.py:105-115: 0 + K_0 + K_1 + ...
+    }
+    __syncthreads();                               // z is rewritten by the next member
     RB_PHASE_MARK(c2);
     RB_PHASE_ADD(1, c1 - c0);
     RB_PHASE_ADD(2, c2 - c1);
-    g = first ? v : g + v;
-    if (last) {
-      if (comp) {
-        T omk = T(0);
+    if (comp) {
+      T omk = T(0);
 #pragma unroll
-        for (int k = 0; k < MAX_MEMBERS; ++k)
-          if (k == mi) omk = om[k];
-        if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
-      } else {
-        total = g;
-      }
+      for (int k = 0; k < MAX_MEMBERS; ++k)
+        if (k == mi) omk = om[k];
+      if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
+    } else {
+      total = g;
     }
+    j0 = j1;
   }
   return total;
 }
