@@ -230,12 +230,12 @@ def run_ours(args):
     fns = [f for f in engine.enabled_ids if fns_req is None or f in fns_req]
     flops = {fn: rotate_flops(engine._pack, fn) for fn in fns}
 
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1001 + rank)
-    x64 = torch.rand((shard.count, D), dtype=torch.float64, device=dev, generator=gen)
-    x64.mul_(200.0).sub_(100.0)
-    x32 = x64.float()
-    xs = {"double": x64, "single": x32}
+    # the §8d population X = Philox(SeedSequence((0, D, N, 1001))).uniform(-100, 100),
+    # drawn on the device bit-identically to numpy; rank r owns its row slice
+    from paper_1407_7737_b200.population import uniform_population, workload_entropy
+    xs = uniform_population(D, shard.count, workload_entropy(D, args.n), first_row=shard.start,
+                            device=local, dtypes=("double", "single"))
+    x64, x32 = xs["double"], xs["single"]
     stream = torch.cuda.current_stream()
 
     per = {}
@@ -360,7 +360,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = x64[: args.cpu_rows * (os.cpu_count() or 1)].cpu().numpy()
+        sample = x64[: args.cpu_rows * (os.cpu_count() or 1)].cpu().numpy()   # rows 0.. of X
         cpu = cpu_reference(D, fns, precs, args.cpu_rows, x_rows=sample)
 
     if args.breakdown and rank == 0:
@@ -372,7 +372,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64+f32" if len(precs) == 2 else ("f64" if precs[0] == "double" else "f32"),
-            "data": "synthetic U[-100,100]^D (torch Philox on device, seed 1001+rank)",
+            "data": ("synthetic X = numpy Philox(SeedSequence((0, D, N, 1001))).uniform(-100, 100), "
+                     "drawn on the device bit-identically (population.py)"),
             "config": {"workload": f"suite-sweep D={D} N={args.n} ({len(fns)} fns x {len(precs)} precisions)",
                        "dim": D, "n": args.n, "fns": len(fns), "precisions": precs,
                        "parallelism": f"rows/{world}", "l2": "inputs larger than L2 (8 GB fp64 + 4 GB fp32)",

@@ -145,6 +145,15 @@ int64_t rb_launch_count(void);
  * semantics (bit-exact SVML powf restatement, csrc/rb_svml_powf.cuh), on
  * device pointers; synchronous on `stream`. */
 rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void* stream);
+/* On-device population source: elements
+ * [first_element, first_element + n_elements) of the stream that
+ * numpy.random.Generator(numpy.random.Philox(key)).uniform(low, high) draws
+ * (Philox4x64-10, key = SeedSequence(...).generate_state(2, uint64)), bit
+ * for bit, into out64 and/or out32 (float32 = the float64 value rounded);
+ * asynchronous on `stream`. */
+rb_status rb_uniform_population(uint64_t key0, uint64_t key1, uint64_t first_element,
+                                int64_t n_elements, double low, double high, double* out64,
+                                float* out32, void* stream);
 /* Diagnostic: clock64() sums of the evaluation kernels of one precision
  * (0 = float64, 1 = float32) over CTAs: [0] tile load, [1] z staging
  * (rotate), [2] kernel values, [3] whole tiles, [4] tiles; zeros unless the

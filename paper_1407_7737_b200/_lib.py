@@ -34,7 +34,7 @@ _STATUS = {
 EXPORTS = ("rb_initialize", "rb_dispose", "rb_func_evaluate", "rb_func_evaluatef",
            "rb_h_func_evaluate", "rb_h_func_evaluatef", "rb_last_error",
            "rb_abi_version", "rb_struct_sizes", "rb_launch_count", "rb_np_powf",
-           "rb_debug_phases")
+           "rb_debug_phases", "rb_uniform_population")
 
 
 class RbPack(ctypes.Structure):
@@ -77,6 +77,10 @@ def load() -> ctypes.CDLL:
     lib.rb_launch_count.restype = i64
     lib.rb_np_powf.argtypes = [vp, vp, vp, i64, vp]
     lib.rb_np_powf.restype = i32
+    u64 = ctypes.c_uint64
+    lib.rb_uniform_population.argtypes = [u64, u64, u64, i64, ctypes.c_double, ctypes.c_double,
+                                          vp, vp, vp]
+    lib.rb_uniform_population.restype = i32
     lib.rb_debug_phases.argtypes = [i32, ctypes.POINTER(ctypes.c_uint64), i32]
     lib.rb_debug_phases.restype = None
     _check_layout(lib)

@@ -28,6 +28,51 @@ cudaError_t set_weier_f32(const float* a_then_c);
 void phase_read_f64(unsigned long long out[8], bool reset);
 void phase_read_f32(unsigned long long out[8], bool reset);
 
+// ------------------------------------------------- on-device population
+// numpy.random.Philox (Philox4x64-10) as numpy runs it: counter starting at
+// 0 and incremented before each 4-word block, key from the SeedSequence;
+// Generator.uniform(low, high) = low + (high - low) * ((u64 >> 11) * 2^-53).
+// Element e of the stream comes from block e / 4 (counter e / 4 + 1), word
+// e % 4, so any row range is generated independently (row-sharded ranks
+// produce exactly their slice of the single-GPU population).
+__device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    const uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += W0;
+    k1 += W1;
+  }
+}
+
+__global__ void uniform_population_kernel(uint64_t k0, uint64_t k1, uint64_t first, int64_t n,
+                                          double low, double high, double* out64, float* out32) {
+  const double range = high - low;
+  const uint64_t b0 = first / 4;                       // first block touched
+  const uint64_t b1 = (first + (uint64_t)n + 3) / 4;   // one past the last
+  for (uint64_t b = b0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < b1;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c[4] = {b + 1, 0, 0, 0};                  // 256-bit counter b + 1 (b < 2^64 - 1)
+    philox4x64_10(c, k0, k1);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint64_t e = b * 4 + w;
+      if (e < first || e >= first + (uint64_t)n) continue;
+      const double u = (double)(c[w] >> 11) * (1.0 / 9007199254740992.0);
+      const double x = low + range * u;
+      if (out64) out64[e - first] = x;
+      if (out32) out32[e - first] = (float)x;
+    }
+  }
+}
+
 __global__ void np_powf_kernel(const float* x, const float* y, float* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -474,6 +519,22 @@ rb_status rb_h_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64
 
 rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f) {
   return evaluate_host<float>(e, fn_id, x, n, f);
+}
+
+rb_status rb_uniform_population(uint64_t key0, uint64_t key1, uint64_t first_element,
+                                int64_t n_elements, double low, double high, double* out64,
+                                float* out32, void* stream) {
+  if (n_elements < 0 || (n_elements > 0 && !out64 && !out32))
+    return fail(RB_E_INVALID_ARGUMENT, "bad arguments");
+  if (n_elements == 0) return RB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = (n_elements + 3) / 4 + 1;
+  const int grid = (int)std::min<int64_t>((blocks + 255) / 256, 148 * 32);
+  rb::uniform_population_kernel<<<grid, 256, 0, st>>>(key0, key1, first_element, n_elements, low,
+                                                        high, out64, out32);
+  g_launches.fetch_add(1);
+  RB_CUDA(cudaGetLastError());
+  return RB_OK;
 }
 
 rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void* stream) {

@@ -599,6 +599,7 @@ struct TileCtx {
   bool x_ready;       // XS holds the X tile
   bool check_z;       // some valid x of the tile is huge or not finite: test every z
   uint32_t live;      // points whose z of the current member are checked
+  bool next_issued;   // single-buffered: the next tile's X copy is already in flight
 };
 
 // X tile into XS (buffer A for fp64); all threads; ends with a barrier.
@@ -607,7 +608,8 @@ template <class T>
 __device__ void fetch_x(const Args<T>& a, const Smem<T>& s, TileCtx& t) {
   PlanHead& P = *s.P;
   if (tile_is_bulk(a, t.nv)) {
-    if (threadIdx.x == 0) issue_tile(a, s.XS, &P.mbar[0], t.tile, t.nv);
+    if (threadIdx.x == 0 && !t.next_issued) issue_tile(a, s.XS, &P.mbar[0], t.tile, t.nv);
+    t.next_issued = false;
     wait_tile(&P.mbar[0], t.phase);
     t.phase ^= 1u;
   } else {
@@ -616,6 +618,19 @@ __device__ void fetch_x(const Args<T>& a, const Smem<T>& s, TileCtx& t) {
   }
   __syncthreads();
   t.x_ready = true;
+}
+
+// Single-buffered X: once the tile's last member is staged (every read of
+// XS is behind the staging barrier) the next tile's copy is started, so it
+// lands while this tile's kernels run.  All threads call it (uniform).
+template <class T>
+__device__ __forceinline__ void issue_next_x(const Args<T>& a, const Smem<T>& s, TileCtx& t) {
+  if (a.nbuf != 1) return;
+  const int64_t ntiles = (a.n + TP - 1) / TP;
+  const int64_t nxt = t.tile + gridDim.x;
+  if (nxt >= ntiles || !tile_is_bulk(a, tile_rows(a, nxt))) return;
+  if (threadIdx.x == 0) issue_tile(a, s.XS, &s.P->mbar[0], nxt, tile_rows(a, nxt));
+  t.next_issued = true;
 }
 
 // ----------------------------------------------------------- one member
@@ -656,11 +671,13 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
 // the calling lane's point: one staging pass, then the chunk kernels in
 // order (hybrid.py:105-115: 0 + K_0 + K_1 + ...).
 template <class T, int KID>
-__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, TileCtx& t) {
+__device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, TileCtx& t,
+                          bool last) {
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
   RB_PHASE_MARK(c0);
   const T* zb = stage_member(a, s, mem, t);
+  if (last) issue_next_x(a, s, t);
   RB_PHASE_MARK(c1);
   T total = T(0);
   for (int si = 0; si < mem.n_segments; ++si) {
@@ -798,7 +815,7 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
     t.live = P.livek[k];
     if (!t.live) continue;
     const rb_member& mem = P.mem[k];
-    const T g = member_value<T, GENERIC>(a, s, mem, t);
+    const T g = member_value<T, GENERIC>(a, s, mem, t, k == nm - 1);
     if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
   }
   return total;
@@ -825,7 +842,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  TileCtx t{0, 0, 0u, false, false, 0u};
+  TileCtx t{0, 0, 0u, false, false, 0u, false};
   uint32_t phase1 = 0u;
   const int64_t first = blockIdx.x;
   const bool f64 = sizeof(T) == 8;
@@ -859,8 +876,10 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
         if (a.nbuf == 2 && next < ntiles && tile_is_bulk(a, tile_rows(a, next)))
           issue_tile(a, b ? s.XB[0] : s.XB[1], b ? &P.mbar[0] : &P.mbar[1], next,
                      tile_rows(a, next));
-        if (a.nbuf == 1 && tile_is_bulk(a, nv)) issue_tile(a, st.XS, &P.mbar[0], tile, nv);
+        if (a.nbuf == 1 && tile_is_bulk(a, nv) && !t.next_issued)
+          issue_tile(a, st.XS, &P.mbar[0], tile, nv);
       }
+      t.next_issued = false;
       if (tile_is_bulk(a, nv)) {
         if (b) {
           wait_tile(&P.mbar[1], phase1);
@@ -899,9 +918,9 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     if constexpr (KID >= SPEC_BASE) {
       result = spec_value<T, KID - SPEC_BASE>(a, st, t, valid);
     } else if constexpr (KID >= 0) {
-      result = member_value<T, KID>(a, st, P.mem[0], t);
+      result = member_value<T, KID>(a, st, P.mem[0], t, true);
     } else if (P.fn.category != RB_COMPOSITION) {
-      result = member_value<T, GENERIC>(a, st, P.mem[0], t);
+      result = member_value<T, GENERIC>(a, st, P.mem[0], t, true);
     } else {
       result = composition_value<T>(a, st, t, valid);
     }

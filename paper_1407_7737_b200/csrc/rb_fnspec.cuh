@@ -116,6 +116,7 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
     const rb_member& mem = P.mem[mi];
     RB_PHASE_MARK(c0);
     const T* zb = stage_member(a, s, mem, t);
+    if (j1 == L.n) issue_next_x(a, s, t);
     RB_PHASE_MARK(c1);
     T g = T(0);
     for (int j = j0; j < j1; ++j) {
