@@ -96,17 +96,24 @@ class EvalResult:
 class Engine:
     """All 37 instances of one (dim, seed), resident on one GPU."""
 
-    def __init__(self, config: EngineConfig):
+    def __init__(self, config: EngineConfig, *, instances=None, enabled=None):
+        """``instances``: {fn: instance} overriding the seeded ones (see
+        fileio.initialize_from_files); ``enabled``: the function ids to
+        build instead of the reference's rule (grid.py needs basic-member
+        compositions at dimension 2, as scalar_evaluator does,
+        engine.py:121-138)."""
         self.config = config
         self._disposed = False
         dim = config.dim
-        if dim >= catalog.MIN_CONSTRUCTED_DIMENSION:
+        if enabled is not None:
+            self._disabled = frozenset(range(catalog.FUNCTION_COUNT)) - frozenset(enabled)
+        elif dim >= catalog.MIN_CONSTRUCTED_DIMENSION:
             self._disabled = frozenset()
         else:                                               # engine.py:148-154
             self._disabled = frozenset(r.fn_id for r in catalog.FUNCTIONS
                                        if r.category in (catalog.HYBRID, catalog.COMPOSITION))
         lib = _lib.load()
-        self._pack = Pack(dim, config.seed, self._disabled)
+        self._pack = Pack(dim, config.seed, self._disabled, instances)
         handle = ctypes.c_void_p()
         _lib.check(lib.rb_initialize(ctypes.byref(_lib.make_pack(self._pack)),
                                      int(config.max_concurrency), int(config.device),

@@ -252,14 +252,17 @@ class _Builder:
 class Pack:
     """Host copy of an ``rb_pack`` (numpy arrays kept alive for the FFI)."""
 
-    def __init__(self, dim: int, seed: int, disabled=frozenset()):
+    def __init__(self, dim: int, seed: int, disabled=frozenset(), overrides=None):
+        """``overrides``: {fn: instance} used instead of regenerating that
+        function's instance from the seed (instances loaded from files)."""
         b = _Builder(dim)
+        overrides = overrides or {}
         for fn in range(catalog.FUNCTION_COUNT):
             rec = b.functions[fn]
             if fn in disabled:
                 rec["category"] = DISABLED
                 continue
-            inst = instances.build(fn, dim, seed)
+            inst = overrides[fn] if fn in overrides else instances.build(fn, dim, seed)
             row = catalog.lookup(fn)
             rec["category"] = CATEGORY[row.category]
             rec["member0"] = len(b.members)
