@@ -325,7 +325,7 @@ def run_ours(args):
         h2d = shard.count * D * 8
         d2h = 0
 
-        def e2e_step():
+        def e2e_step_plain():
             nonlocal d2h
             d2h = 0
             dev_x.copy_(host_x, non_blocking=True)
@@ -338,6 +338,53 @@ def run_ours(args):
                     dst.copy_(full, non_blocking=True)
                     d2h += full.numel() * full.element_size()
             torch.cuda.synchronize()
+
+        # one GPU: a chunked pipeline -- the H2D copy of row chunk c+1 and the
+        # D2H of chunk c-1's fitness values run on a copy stream while chunk c
+        # is evaluated (every function, both precisions; values land in a
+        # resident results buffer through Engine.evaluate(out=...))
+        n_chunks = 8 if world == 1 and shard.count >= 8 * 4096 else 1
+        bounds = [shard.count * c // n_chunks for c in range(n_chunks + 1)]
+        nc_max = max(bounds[c + 1] - bounds[c] for c in range(n_chunks))
+        copy_stream = torch.cuda.Stream(device=dev)
+        res = {p: torch.empty((2, len(fns), nc_max), dtype=torch.float64 if p == "double" else torch.float32,
+                              device=dev) for p in precs}
+        host_res = {p: torch.empty((2, len(fns), nc_max), dtype=res[p].dtype, pin_memory=True)
+                    for p in precs}
+
+        def e2e_step_pipelined():
+            nonlocal d2h
+            d2h = 0
+            ev_in = [torch.cuda.Event() for _ in range(n_chunks)]
+            ev_done = [torch.cuda.Event() for _ in range(n_chunks)]
+            ev_out = [torch.cuda.Event() for _ in range(n_chunks)]
+            with torch.cuda.stream(copy_stream):
+                for c in range(n_chunks):
+                    lo_, hi_ = bounds[c], bounds[c + 1]
+                    dev_x[lo_:hi_].copy_(host_x[lo_:hi_], non_blocking=True)
+                    ev_in[c].record(copy_stream)
+            for c in range(n_chunks):
+                lo_, hi_ = bounds[c], bounds[c + 1]
+                nc = hi_ - lo_
+                stream.wait_event(ev_in[c])
+                if c >= 2:
+                    stream.wait_event(ev_out[c - 2])        # results slot c % 2 copied out
+                xc = dev_x[lo_:hi_]
+                xcs = {"double": xc, "single": xc.float()}
+                for p in precs:
+                    for i, fn in enumerate(fns):
+                        engine.evaluate(fn, xcs[p], p, out=res[p][c % 2, i, :nc])
+                ev_done[c].record(stream)
+                with torch.cuda.stream(copy_stream):
+                    copy_stream.wait_event(ev_done[c])
+                    for p in precs:
+                        host_res[p][c % 2, :, :nc].copy_(res[p][c % 2, :, :nc], non_blocking=True)
+                        d2h += len(fns) * nc * res[p].element_size()
+                    ev_out[c].record(copy_stream)
+            stream.wait_stream(copy_stream)
+            torch.cuda.synchronize()
+
+        e2e_step = e2e_step_pipelined if world == 1 else e2e_step_plain
 
         e2e_step()
         barrier()
@@ -355,8 +402,11 @@ def run_ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
         e2e = {"value": evals / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps}
-        del host_x, host_f
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
+               "pipeline": (f"{n_chunks} row chunks: H2D of X and D2H of every fitness vector on a "
+                            "copy stream, overlapped with evaluation" if world == 1 else
+                            "H2D, evaluate + NCCL all-gather, D2H per function")}
+        del host_x, host_f, host_res, res
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

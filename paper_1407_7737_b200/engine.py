@@ -132,8 +132,12 @@ class Engine:
     def enabled_ids(self) -> tuple:
         return tuple(fn for fn in range(catalog.FUNCTION_COUNT) if fn not in self._disabled)
 
-    def evaluate(self, fn_id: int, batch, precision: str | None = None) -> EvalResult:
-        """Score every point of ``batch`` against ``fn_id`` (engine.py:174-214)."""
+    def evaluate(self, fn_id: int, batch, precision: str | None = None, *, out=None) -> EvalResult:
+        """Score every point of ``batch`` against ``fn_id`` (engine.py:174-214).
+
+        ``out`` (addition, CUDA batches only): a contiguous device tensor of
+        the batch's length and the precision's dtype that receives the values
+        (pipelines that keep results resident, e.g. bench.py's e2e step)."""
         if self._disposed:
             raise UseAfterDispose("engine was disposed")
         if not isinstance(batch, PointBatch):
@@ -152,7 +156,9 @@ class Engine:
         if precision not in _DTYPES:
             raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
         if _is_torch(batch.data):
-            return EvalResult(self._evaluate_device(fn_id, batch.data, precision))
+            return EvalResult(self._evaluate_device(fn_id, batch.data, precision, out))
+        if out is not None:
+            raise ValueError("out= is only supported for CUDA tensor batches")
         return EvalResult(self._evaluate_host(fn_id, batch.data, precision))
 
     def evaluate_single_precision(self, fn_id: int, batch) -> EvalResult:
@@ -180,13 +186,17 @@ class Engine:
         _lib.check(call(self._handle, fn_id, _lib.ptr(pts), pts.shape[0], _lib.ptr(out)))
         return out
 
-    def _evaluate_device(self, fn_id, data, precision):
+    def _evaluate_device(self, fn_id, data, precision, out=None):
         import torch
         if not data.is_cuda or data.device.index != self.config.device:
             raise ValueError(f"tensor must live on cuda:{self.config.device}")
         dt = torch.float64 if precision == "double" else torch.float32
         pts = data.to(dt).contiguous()
-        out = torch.empty(pts.shape[0], dtype=dt, device=pts.device)
+        if out is None:
+            out = torch.empty(pts.shape[0], dtype=dt, device=pts.device)
+        elif (out.dtype != dt or out.device != pts.device or not out.is_contiguous()
+              or out.numel() != pts.shape[0]):
+            raise ValueError("out must be a contiguous device tensor of the batch's length and dtype")
         stream = torch.cuda.current_stream(pts.device).cuda_stream
         call = _lib.load().rb_func_evaluate if dt == torch.float64 else _lib.load().rb_func_evaluatef
         _lib.check(call(self._handle, fn_id, pts.data_ptr(), pts.shape[0], out.data_ptr(), stream))
