@@ -153,14 +153,16 @@ def _cpu_worker(job):
     return n, time.perf_counter() - t0
 
 
-def cpu_reference(dim, fns, precs, rows_per_proc, x_rows=None, procs=None):
+def cpu_reference(dim, fns, precs, rows_per_proc, x_rows=None, procs=None, n_total=None):
     """The reference's per-point path (oracle port, bit-identical to
-    robench) on every host core: P processes over disjoint row slices."""
+    robench) on every host core: P processes over disjoint row slices of the
+    first rows of the §8d population."""
     import multiprocessing as mp
     procs = procs or os.cpu_count() or 1
     if x_rows is None:
-        rng = np.random.default_rng(1001)
-        x_rows = rng.uniform(-100.0, 100.0, (rows_per_proc * procs, dim))
+        from paper_1407_7737_b200.population import host_rows, workload_entropy
+        x_rows = host_rows(dim, workload_entropy(dim, n_total or rows_per_proc * procs), 0,
+                           rows_per_proc * procs)
     jobs = [(dim, fns, precs, x_rows[i * rows_per_proc:(i + 1) * rows_per_proc])
             for i in range(procs)]
     ctx = mp.get_context("fork")
@@ -182,8 +184,8 @@ def run_reference(args):
     fns = list(range(37)) if args.fns == "all" else [int(f) for f in args.fns.split(",")]
     precs = [p for p in args.precisions.split(",")]
     for _ in range(max(args.warmup, 0)):
-        cpu_reference(args.dim, fns, precs, max(2, args.cpu_rows // 8))
-    vals = [cpu_reference(args.dim, fns, precs, args.cpu_rows) for _ in range(args.steps)]
+        cpu_reference(args.dim, fns, precs, max(2, args.cpu_rows // 8), n_total=args.n)
+    vals = [cpu_reference(args.dim, fns, precs, args.cpu_rows, n_total=args.n) for _ in range(args.steps)]
     cores = vals[0]["cores"]
     value = statistics.median(v["value"] for v in vals)
     line = {
@@ -191,7 +193,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * 37 * len(precs) * args.n / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64+f32", "data": "synthetic U[-100,100]^D",
+        "dtype": "f64+f32",
+        "data": "synthetic X = numpy Philox(SeedSequence((0, D, N, 1001))).uniform(-100, 100), first rows",
         "config": {"workload": f"suite-sweep D={args.dim} N={args.n} (37 fns x {len(precs)} precisions)",
                    "dim": args.dim, "n": args.n, "fns": len(fns), "precisions": precs,
                    "sample": vals[0]["sample"]},
