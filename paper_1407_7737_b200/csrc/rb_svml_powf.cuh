@@ -39,7 +39,9 @@
 #endif
 
 #if defined(__CUDACC__)
-#define RB_SVML_TAB __device__ __constant__ const
+// global (L1-cached) rather than __constant__: the lookups are indexed by
+// each lane's own mantissa bits, and divergent constant-bank reads serialise
+#define RB_SVML_TAB static __device__ const
 #else
 #define RB_SVML_TAB static const
 #endif
