@@ -197,9 +197,13 @@ __device__ __forceinline__ T kernel_value_k(const Pt<T>& P) {
     // float64 its reciprocal (multiplied by, to tolerance) -- pack.py
     const T* sq_i = P.ctab;
     const T s = pw8<T>(0, d, square, l8);
-    const T p = prod8<T>(d, [&](int i) {
+    auto factor = [&](int i) {
       return M<T>::cos(sizeof(T) == 8 ? z[i] * sq_i[i] : z[i] / sq_i[i]);
-    }, l8);
+    };
+    // fp32: the left fold of np.prod through shared memory (the sum above
+    // has read z already); fp64: lane partial products
+    const T p = sizeof(T) == 4 ? prod8_fold<T>(d, factor, l8, const_cast<T*>(z))
+                               : prod8<T>(d, factor, l8);
     return (s / C<T>(4000.0) - p) + C<T>(1.0);
   } else if constexpr (K == K_RASTRIGIN) {                            // :115-117
     return pw8<T>(0, d, [&](int i) {

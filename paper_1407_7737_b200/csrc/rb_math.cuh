@@ -197,6 +197,20 @@ __device__ __forceinline__ T pw8(int lo, int n, F&& f, int l8) {
 // Sequential product over i = 0..n-1 of f(i) (np.prod is a plain left fold,
 // kernels.py:112); lane l8 evaluates the i = l8 (mod 8) factors.  float64
 // multiplies lane partials instead (order-free to its tolerance).
+// float32 np.prod without a shuffle chain: every lane writes its factors
+// over its own elements of the point's z row (each element is read and
+// rewritten by the same lane, and z is dead after the product), then lane 0
+// folds the row left to right and broadcasts.  ``scratch`` = the z row.
+template <class T, class F>
+__device__ __forceinline__ T prod8_fold(int n, F&& f, int l8, T* scratch) {
+  for (int i = l8; i < n; i += 8) scratch[i] = f(i);
+  __syncwarp();
+  T p = T(1);
+  if (l8 == 0)
+    for (int i = 0; i < n; ++i) p = p * scratch[i];
+  return __shfl_sync(RB_FULL, p, 0, 8);
+}
+
 template <class T, class F>
 __device__ __forceinline__ T prod8(int n, F&& f, int l8) {
   if constexpr (sizeof(T) == 8) {        // float64: lane partial products, butterfly
