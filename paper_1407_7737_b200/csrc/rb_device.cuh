@@ -372,11 +372,16 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
 // b = (tig, gid), c_i = (gid + 8*(i>>1), 2*tig + (i&1)).
 // R (1 or 2) n-tiles of one (group, m-tile) over all k-steps: A = x - o
 // gathered through the column table, B pre-swizzled from the pack.
+#ifndef RB_DMMA_UNROLL
+#define RB_DMMA_UNROLL 3
+#endif
+constexpr int kDmmaUnroll = RB_DMMA_UNROLL;
+
 template <int R>
 __device__ __forceinline__ void dmma_run(const double* X0, const double* X1, const int* qs,
                                          const double* qo, const double* F, int nks,
                                          double (&acc)[2][4]) {
-#pragma unroll 3
+#pragma unroll kDmmaUnroll
   for (int ks = 0; ks < nks; ++ks) {
     const int col = qs[ks * 4];
     const double o = qo[ks * 4];

@@ -65,3 +65,29 @@ def test_shard_partition():
             shards = [Shard(r, w, n) for r in range(w)]
             assert sum(s.count for s in shards) == n
             assert [s.start for s in shards] == list(np.cumsum([0] + [s.count for s in shards])[:-1])
+
+
+def _pop_worker(rank, world, port, dim, n, out):
+    # each rank draws only its shard of the 8d population (what bench.py does
+    # on the device with population.uniform_population(first_row=shard.start))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1407_7737_b200.dist import gather_fitness
+    from paper_1407_7737_b200.population import host_rows, workload_entropy
+    sh = Shard(rank, world, n)
+    local = torch.from_numpy(host_rows(dim, workload_entropy(dim, n), sh.start, sh.count)).reshape(-1)
+    rows = [torch.empty(c * dim, dtype=torch.float64) for c in sh.sizes]
+    dist.all_gather(rows, local)
+    if rank == 0:
+        np.save(out, torch.cat(rows).numpy().reshape(n, dim))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 12), (4, 10)])
+def test_sharded_population_is_the_single_process_draw(tmp_path, world, n):
+    from paper_1407_7737_b200.population import workload_entropy
+    out = str(tmp_path / "x.npy")
+    mp.spawn(_pop_worker, args=(world, free_port(), 100, n, out), nprocs=world, join=True)
+    want = np.random.Generator(np.random.Philox(np.random.SeedSequence(
+        workload_entropy(100, n)))).uniform(-100, 100, (n, 100))
+    assert np.array_equal(np.load(out), want)
