@@ -72,14 +72,17 @@ def _pop_worker(rank, world, port, dim, n, out):
     # on the device with population.uniform_population(first_row=shard.start))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1407_7737_b200.dist import gather_fitness
     from paper_1407_7737_b200.population import host_rows, workload_entropy
     sh = Shard(rank, world, n)
     local = torch.from_numpy(host_rows(dim, workload_entropy(dim, n), sh.start, sh.count)).reshape(-1)
-    rows = [torch.empty(c * dim, dtype=torch.float64) for c in sh.sizes]
-    dist.all_gather(rows, local)
+    width = max(sh.sizes) * dim                       # gloo gathers equal sizes: pad
+    padded = torch.zeros(width, dtype=torch.float64)
+    padded[: local.numel()] = local
+    rows = [torch.empty(width, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(rows, padded)
     if rank == 0:
-        np.save(out, torch.cat(rows).numpy().reshape(n, dim))
+        full = torch.cat([rows[r][: c * dim] for r, c in enumerate(sh.sizes)])
+        np.save(out, full.numpy().reshape(n, dim))
     dist.destroy_process_group()
 
 
