@@ -95,9 +95,11 @@ template <class T> __device__ __forceinline__ T katsuura_row(T zj) {
   for (int i = 0; i < 32; ++i) {
     const T p2 = T(1ull << (i + 1));  // 2**(i+1), exact
     const T w = p2 * zj;
-    // "/ 2**(i+1)" as a product with the exact reciprocal: both are the
-    // correctly rounded scaling of the same value (no division sequence)
-    r[i & 7] = r[i & 7] + M<T>::fabs(w - M<T>::floor(w + C<T>(0.5))) * T(1.0 / double(1ull << (i + 1)));
+    // floor(w + 0.5) exactly as the reference rounds it (w + 0.5 itself
+    // rounds for |w| >= 2^52 / 2^23).  d * 2**-(i+1) is an exact scaling, so
+    // the FMA rounds the sum exactly like "/ 2**(i+1)" followed by "+".
+    const T d = M<T>::fabs(w - M<T>::floor(w + C<T>(0.5)));
+    r[i & 7] = M<T>::fma(d, T(1.0 / double(1ull << (i + 1))), r[i & 7]);
   }
   return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
 }

@@ -34,6 +34,7 @@ template <> struct M<double> {
   static __device__ __forceinline__ double fabs(double x) { return ::fabs(x); }
   static __device__ __forceinline__ double fmod(double x, double y) { return ::fmod(x, y); }
   static __device__ __forceinline__ double trunc(double x) { return ::trunc(x); }
+  static __device__ __forceinline__ double rint(double x) { return ::rint(x); }
   static __device__ __forceinline__ double fma(double a, double b, double c) { return ::fma(a, b, c); }
   static __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 };
@@ -57,6 +58,7 @@ template <> struct M<float> {
   static __device__ __forceinline__ float fabs(float x) { return ::fabsf(x); }
   static __device__ __forceinline__ float fmod(float x, float y) { return ::fmodf(x, y); }
   static __device__ __forceinline__ float trunc(float x) { return ::truncf(x); }
+  static __device__ __forceinline__ float rint(float x) { return ::rintf(x); }
   static __device__ __forceinline__ float fma(float a, float b, float c) { return ::fmaf(a, b, c); }
   static __device__ __forceinline__ bool finite(float x) { return isfinite(x); }
 };
