@@ -25,9 +25,6 @@
 #include "../../include/robench_b200.h"
 #include "rb_kernels.cuh"
 
-#ifndef RB_NTC
-#define RB_NTC 2
-#endif
 #ifndef RB_MIN_BLOCKS_F64
 #define RB_MIN_BLOCKS_F64 3
 #endif
@@ -61,11 +58,7 @@ constexpr int MAX_MEMBERS = 5;
 constexpr int MAX_SEGMENTS = 16;
 constexpr int MAX_GROUPS = 16;
 constexpr int MAX_UNITS = 512;  // fp64 DMMA units (m-tile x n-tile of a group) per function
-constexpr int NTC = RB_NTC;     // DMMA n-tiles (8 rows) accumulated per pass
-#ifndef RB_KB
-#define RB_KB 1
-#endif
-constexpr int KB = RB_KB;       // fp64 rotate: k-steps whose operands are loaded ahead
+constexpr int NTC = 2;          // DMMA n-tiles (8 rows) sharing one A fragment per k-step
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
 template <class T>
@@ -411,7 +404,7 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
     const int g = ud & 0xff, mt = (ud >> 8) & 0xff, nt0 = ud >> 16;
     const rb_group& G = P.grp[g];
     const int m = G.m, ntn = (m + 7) >> 3, nks = (m + 3) >> 2;
-    const int run = min(min(2, ntn - nt0), end - u);
+    const int run = min(min(NTC, ntn - nt0), end - u);
     const double* F = a.values + G.frag + (size_t)nt0 * nks * 32 + lane;
     const int* qs = s.qsrc + P.gq0[g] + tig;    // padded columns read x[.][0] * B = 0
     const double* qo = s.qo + P.gq0[g] + tig;
@@ -601,7 +594,6 @@ struct TileCtx {
   int64_t tile;
   int nv;             // valid rows
   uint32_t phase;     // parity of mbar[0] (fp64 loads / refetches)
-  bool x_ready;       // XS holds the X tile
   bool check_z;       // some valid x of the tile is huge or not finite: test every z
   uint32_t live;      // points whose z of the current member are checked
   bool next_issued;   // single-buffered: the next tile's X copy is already in flight
@@ -622,7 +614,6 @@ __device__ void fetch_x(const Args<T>& a, const Smem<T>& s, TileCtx& t) {
     for (int e = threadIdx.x; e < t.nv * a.dim; e += NT) s.XS[e] = src[e];
   }
   __syncthreads();
-  t.x_ready = true;
 }
 
 // Single-buffered X: once the tile's last member is staged (every read of
@@ -847,7 +838,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  TileCtx t{0, 0, 0u, false, false, 0u, false};
+  TileCtx t{0, 0, 0u, false, 0u, false};
   uint32_t phase1 = 0u;
   const int64_t first = blockIdx.x;
   const bool f64 = sizeof(T) == 8;
@@ -898,7 +889,6 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
         for (int e = threadIdx.x; e < nv * a.dim; e += NT) st.XS[e] = src[e];
       }
       __syncthreads();
-      t.x_ready = true;
     }
     // engine.py:202-203: a non-finite x anywhere in the batch raises; a
     // finite but huge x can still overflow z (kernels.py:45-49), so such
