@@ -462,31 +462,43 @@ __device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, 
 // Exact NumPy order (transforms.py:42-48): rounded products, per-slot
 // accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
 // ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
+// gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre   (engine.py:97-100)
+// for the groups of plan segments [s_first, s_end).  Every x of the tile is
+// read here once per member, so it also returns the max |x| bit pattern over
+// the valid points (the X scan of evaluate_kernel, folded in; nv = 0: skip).
+__device__ inline uint32_t gather_v(const Args<float>& a, const Smem<float>& s, int s_first,
+                                    int s_end, int nv) {
+  const PlanHead& P = *s.P;
+  const int g0 = P.seg[s_first].group0 - P.grp_base;
+  const int ng = P.seg[s_end - 1].group0 + P.seg[s_end - 1].n_groups - P.seg[s_first].group0;
+  uint32_t mx = 0u;
+  int vq = 0;
+  for (int g = 0; g < ng; ++g) {
+    const rb_segment& sg = P.seg[P.grp_seg[g0 + g]];
+    const float scale = (float)sg.scale, pre = (float)sg.pre;
+    const int kp = round4(P.grp[g0 + g].m);
+    const int* qs = s.qsrc + P.gq0[g0 + g];
+    const float* qo = s.qo + P.gq0[g0 + g];
+    for (int e = threadIdx.x; e < TP * kp; e += NT) {
+      const int q = e / TP, p = e - q * TP;
+      const float x = s.XS[p * a.dim + qs[q]];
+      if (p < nv) mx = max(mx, __float_as_uint(x) & 0x7fffffffu);
+      float v = scale * (x - qo[q]);
+      if (pre != 0.0f) v = v + pre;
+      s.VS[(vq + q) * TP + p] = v;
+    }
+    vq += kp;
+  }
+  return mx;
+}
+
+// the V tile is in place (gather_v + barrier)
 template <bool CHECK>
 __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, int s_first,
                                   int s_end) {
   const PlanHead& P = *s.P;
   const int g0 = P.seg[s_first].group0 - P.grp_base;
   const int ng = P.seg[s_end - 1].group0 + P.seg[s_end - 1].n_groups - P.seg[s_first].group0;
-  // gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre   (engine.py:97-100)
-  {
-    int vq = 0;
-    for (int g = 0; g < ng; ++g) {
-      const rb_segment& sg = P.seg[P.grp_seg[g0 + g]];
-      const float scale = (float)sg.scale, pre = (float)sg.pre;
-      const int kp = round4(P.grp[g0 + g].m);
-      const int* qs = s.qsrc + P.gq0[g0 + g];
-      const float* qo = s.qo + P.gq0[g0 + g];
-      for (int e = threadIdx.x; e < TP * kp; e += NT) {
-        const int q = e / TP, p = e - q * TP;
-        float v = scale * (s.XS[p * a.dim + qs[q]] - qo[q]);
-        if (pre != 0.0f) v = v + pre;
-        s.VS[(vq + q) * TP + p] = v;
-      }
-      vq += kp;
-    }
-  }
-  __syncthreads();
   int total = 0;
   for (int g = 0; g < ng; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
   uint32_t nf = 0u;
@@ -595,6 +607,7 @@ struct TileCtx {
   int nv;             // valid rows
   uint32_t phase;     // parity of mbar[0] (fp64 loads / refetches)
   bool check_z;       // some valid x of the tile is huge or not finite: test every z
+  bool scanned;       // the tile's X scan is done (fp32: folded into the first gather)
   uint32_t live;      // points whose z of the current member are checked
   bool next_issued;   // single-buffered: the next tile's X copy is already in flight
 };
@@ -656,6 +669,16 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
       if (t.check_z && not_finite(v)) nf |= 1u << p;
     }
   } else {
+    if constexpr (sizeof(T) == 4) {
+      const uint32_t mx = gather_v(a, s, s_first, s_end, t.scanned ? 0 : t.nv);
+      if (!t.scanned) {                    // X scan of this tile (see evaluate_kernel)
+        if (mx >= 0x7f800000u) atomicOr(a.flag, 2);
+        t.check_z = __syncthreads_or(mx >= 0x71800000u) != 0;
+        t.scanned = true;
+      } else {
+        __syncthreads();
+      }
+    }
     nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
   }
   if (nf & t.live) atomicOr(a.flag, 2);
@@ -838,7 +861,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
-  TileCtx t{0, 0, 0u, false, 0u, false};
+  TileCtx t{0, 0, 0u, false, false, 0u, false};
   uint32_t phase1 = 0u;
   const int64_t first = blockIdx.x;
   const bool f64 = sizeof(T) == 8;
@@ -894,7 +917,10 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     // finite but huge x can still overflow z (kernels.py:45-49), so such
     // tiles test every z they produce.
     const bool valid = p < nv;
-    {
+    // fp32 functions whose first stage is rotated fold the scan into that
+    // stage's V gather (gather_v), which reads every x anyway
+    t.scanned = !(sizeof(T) == 4 && P.seg[0].n_groups > 0);
+    if (t.scanned) {
       // max of |x| bit patterns (high word for float64) over the point's row
       uint32_t mx = 0u;
       if (valid) {
