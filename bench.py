@@ -350,10 +350,12 @@ def run_ours(args):
         bounds = [shard.count * c // n_chunks for c in range(n_chunks + 1)]
         nc_max = max(bounds[c + 1] - bounds[c] for c in range(n_chunks))
         copy_stream = torch.cuda.Stream(device=dev)
-        res = {p: torch.empty((2, len(fns), nc_max), dtype=torch.float64 if p == "double" else torch.float32,
-                              device=dev) for p in precs}
-        host_res = {p: torch.empty((2, len(fns), nc_max), dtype=res[p].dtype, pin_memory=True)
-                    for p in precs}
+        res, host_res = {}, {}
+        if world == 1:                    # resident results of two chunks in flight
+            res = {p: torch.empty((2, len(fns), nc_max), device=dev,
+                                  dtype=torch.float64 if p == "double" else torch.float32) for p in precs}
+            host_res = {p: torch.empty((2, len(fns), nc_max), dtype=res[p].dtype, pin_memory=True)
+                        for p in precs}
 
         def e2e_step_pipelined():
             nonlocal d2h
