@@ -316,6 +316,12 @@ def run_ours(args):
                         "profiles/peaks_r01.json (tools/peaks_microbench.cu on this pool: "
                         + ("DMMA m16n8k4 f64" if dom["precision"] == "double" else "FMUL+FADD f32") + ")"),
         "suite_frac": sum(max(r["t_roof_hbm"], r["t_roof_fp"]) for r in rows) / sum(r["seconds"] for r in rows),
+        # the compute bound is the rotation's 2*nnz flops: DMMA (tensor
+        # pipe) in fp64; exact-order SIMT FMUL+FADD in fp32 (NumPy's rounding rules out
+        # FMA and TF32 tensor cores); transcendental work is outside F (pipe
+        # utilisation in profiles/)
+        "compute_pipe": ("fp64 DMMA (mma.sync m16n8k4)" if dom["precision"] == "double"
+                         else "fp32 SIMT FMUL+FADD, exact NumPy order"),
     }
 
     # e2e through the public API from pinned host memory
