@@ -68,6 +68,9 @@ typedef struct rb_group {
                        computes z_r = sum_q (scale B)[q][r] (x[src_q] - o[src_q]) - cz[r] */
   int32_t col64;    /* index[col64 + q]: input position of the q-th float64 column (an order
                        whose 4-column k-steps read shared memory without bank conflicts) */
+  int32_t leaf;     /* -1: one pairwise leaf (qb above).  Else index[leaf ...] = [n_leaf (2 or 3),
+                       qb of leaf 0, 1(, 2) (10 ints each, absolute q)]: float32 rows of length
+                       129..256 are summed as NumPy's tree l0 + l1 or l0 + (l1 + l2) */
 } rb_group;
 
 /* One kernel application: v = scale*((x - o)[src..]) + pre; z = R v + post;

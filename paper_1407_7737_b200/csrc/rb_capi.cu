@@ -210,7 +210,7 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   if (n < 1 || !x || !f) return fail(RB_E_INVALID_ARGUMENT, "empty batch or null pointer");
   const int pi = sizeof(T) == 8 ? 0 : 1;
   if (pi == 1 && !e->exact_ok[fn_id])
-    return fail(RB_E_UNSUPPORTED, "single precision needs rotation blocks of length <= 128");
+    return fail(RB_E_UNSUPPORTED, "single precision needs rotation blocks of length <= 256");
   const Launch& L = e->launch[pi][fn_id];
 
   int prev = 0;
@@ -321,7 +321,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
           q4 += (pk->groups[g].m + 3) & ~3;
           units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
         }
-        if (sg.n_groups && sg.d > 128) e->exact_ok[fi] = 0;
+        if (sg.n_groups && sg.d > 256) e->exact_ok[fi] = 0;
       }
       ldv = std::max(ldv, q4);
     }

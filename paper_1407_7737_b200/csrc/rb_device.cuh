@@ -492,6 +492,74 @@ __device__ inline uint32_t gather_v(const Args<float>& a, const Smem<float>& s, 
   return mx;
 }
 
+// One pairwise leaf of the float32 exact-order rotate for RR block rows and
+// the 4 points of a float4 V column: slot s walks q in [qb[s], qb[s+1]) with
+// FMUL + FADD (NumPy's r[s] += a[i] per slot), the 8 slots fold as
+// ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)) and the tail adds in order
+// (SURVEY.md Appendix A).  bp: B row qb[0] (rows r0.., stride m4).
+template <int RR>
+__device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int bstride,
+                                         const int (&qb)[10], float (&t0)[4][RR]) {
+  constexpr int vstride = TP / 4;
+  float t1[4][RR], t2[4][RR], acc[4][RR];
+  auto load_b = [&](const float* b, float (&bb)[RR]) {
+    if constexpr (RR == 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(b));
+      bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
+    } else {
+      const float2 v = __ldg(reinterpret_cast<const float2*>(b));
+      bb[0] = v.x; bb[1] = v.y;
+    }
+  };
+#pragma unroll
+  for (int sl = 0; sl < 8; ++sl) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) acc[i][j] = 0.0f;
+#pragma unroll 2
+    for (int q = qb[sl]; q < qb[sl + 1]; ++q, bp += bstride) {
+      const float4 v = Vq[q * vstride];
+      float bb[RR];
+      load_b(bp, bb);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < RR; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(vv[i], bb[j]));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) {
+        const float x = acc[i][j];
+        switch (sl) {
+          case 0: t0[i][j] = x; break;
+          case 1: t0[i][j] = __fadd_rn(t0[i][j], x); break;
+          case 2: t1[i][j] = x; break;
+          case 3: t1[i][j] = __fadd_rn(t1[i][j], x); t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]); break;
+          case 4: t1[i][j] = x; break;
+          case 5: t1[i][j] = __fadd_rn(t1[i][j], x); break;
+          case 6: t2[i][j] = x; break;
+          default:
+            t2[i][j] = __fadd_rn(t2[i][j], x);
+            t1[i][j] = __fadd_rn(t1[i][j], t2[i][j]);
+            t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]);
+        }
+      }
+  }
+  for (int q = qb[8]; q < qb[9]; ++q, bp += bstride) {
+    const float4 v = Vq[q * vstride];
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    float bb[RR];
+    load_b(bp, bb);
+#pragma unroll
+    for (int j = 0; j < RR; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], bb[j]));
+  }
+}
+
 // the V tile is in place (gather_v + barrier)
 template <bool CHECK>
 __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, int s_first,
@@ -516,84 +584,66 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
     const int pq = rem % (TP / 4), rq = rem / (TP / 4);
     const int m = G.m, m4 = round4(m);
     const int* prow = s.prow + P.gq0[g];
-    constexpr int RR = RB_F32_ROWS;
-#pragma unroll 1
-    for (int pass = 0; pass < 4 / RR; ++pass) {
-      const int r0 = rq * 4 + pass * RR;
-      if (r0 >= m) break;
-      const float* B = a.values + G.mat + r0;
-      // column q: V row vq + q (4 points, one float4) and B row q (RR rows)
-      const float4* Vq = reinterpret_cast<const float4*>(s.VS + vq * TP + pq * 4);
-      constexpr int vstride = TP / 4;
-      const int bstride = m4;
+    // column q: V row vq + q (4 points, one float4) and B row q
+    const float4* Vq = reinterpret_cast<const float4*>(s.VS + vq * TP + pq * 4);
+    if (G.leaf < 0) {                          // one pairwise leaf (m <= 128)
+      constexpr int RR = RB_F32_ROWS;
       int qb[10];
 #pragma unroll
       for (int k = 0; k < 10; ++k) qb[k] = G.qb[k];
-      float t0[4][RR], t1[4][RR], t2[4][RR], acc[4][RR];
-      auto load_b = [&](const float* bp, float (&bb)[RR]) {
-        if constexpr (RR == 4) {
-          const float4 b = __ldg(reinterpret_cast<const float4*>(bp));
-          bb[0] = b.x; bb[1] = b.y; bb[2] = b.z; bb[3] = b.w;
-        } else {
-          const float2 b = __ldg(reinterpret_cast<const float2*>(bp));
-          bb[0] = b.x; bb[1] = b.y;
+#pragma unroll 1
+      for (int pass = 0; pass < 4 / RR; ++pass) {
+        const int r0 = rq * 4 + pass * RR;
+        if (r0 >= m) break;
+        float z[4][RR];
+        f32_leaf<RR>(Vq, a.values + G.mat + r0, m4, qb, z);
+#pragma unroll
+        for (int j = 0; j < RR; ++j) {
+          if (r0 + j >= m) break;
+          const int row = prow[r0 + j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            put_z<CHECK>(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(z[i][j], post) : z[i][j], nf);
         }
-      };
-      const float* bp = B;                       // B row q, advanced with q
+      }
+    } else {
+      // 129..256: NumPy's tree over 2 or 3 leaves, l0 + l1 or l0 + (l1 + l2)
+      constexpr int RR = 2;
+      const int* L = a.index + G.leaf;
+      const int nl = __ldg(L);
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int r0 = rq * 4 + pass * RR;
+        if (r0 >= m) break;
+        const float* B = a.values + G.mat + r0;
+        float z[4][RR], u[4][RR];
+        int qb[10];
 #pragma unroll
-      for (int sl = 0; sl < 8; ++sl) {
+        for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 1 + k);
+        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, z);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 11 + k);
+        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, u);
+        if (nl == 3) {
+          float w[4][RR];
 #pragma unroll
-          for (int j = 0; j < RR; ++j) acc[i][j] = 0.0f;
-#pragma unroll 2
-        for (int q = qb[sl]; q < qb[sl + 1]; ++q, bp += bstride) {
-          const float4 v = Vq[q * vstride];
-          float bb[RR];
-          load_b(bp, bb);
-          const float vv[4] = {v.x, v.y, v.z, v.w};
+          for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 21 + k);
+          f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, w);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < RR; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(vv[i], bb[j]));
+            for (int j = 0; j < RR; ++j) u[i][j] = __fadd_rn(u[i][j], w[i][j]);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < RR; ++j) {
+          if (r0 + j >= m) break;
+          const int row = prow[r0 + j];
 #pragma unroll
-          for (int j = 0; j < RR; ++j) {
-            const float x = acc[i][j];
-            switch (sl) {
-              case 0: t0[i][j] = x; break;
-              case 1: t0[i][j] = __fadd_rn(t0[i][j], x); break;
-              case 2: t1[i][j] = x; break;
-              case 3: t1[i][j] = __fadd_rn(t1[i][j], x); t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]); break;
-              case 4: t1[i][j] = x; break;
-              case 5: t1[i][j] = __fadd_rn(t1[i][j], x); break;
-              case 6: t2[i][j] = x; break;
-              default:
-                t2[i][j] = __fadd_rn(t2[i][j], x);
-                t1[i][j] = __fadd_rn(t1[i][j], t2[i][j]);
-                t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]);
-            }
+          for (int i = 0; i < 4; ++i) {
+            const float zz = __fadd_rn(z[i][j], u[i][j]);
+            put_z<CHECK>(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(zz, post) : zz, nf);
           }
-      }
-      for (int q = qb[8]; q < qb[9]; ++q, bp += bstride) {
-        const float4 v = Vq[q * vstride];
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        float bb[RR];
-        load_b(bp, bb);
-#pragma unroll
-        for (int j = 0; j < RR; ++j)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], bb[j]));
-      }
-#pragma unroll
-      for (int j = 0; j < RR; ++j) {
-        if (r0 + j >= m) break;
-        const int row = prow[r0 + j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          put_z<CHECK>(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(t0[i][j], post) : t0[i][j], nf);
+        }
       }
     }
   }

@@ -31,7 +31,7 @@ from . import catalog, instances
 
 GROUP_DT = np.dtype([("m", "<i4"), ("qb", "<i4", (10,)), ("col", "<i4"),
                      ("row", "<i4"), ("mat", "<i4"), ("frag", "<i4"), ("cz", "<i4"),
-                     ("col64", "<i4")])
+                     ("col64", "<i4"), ("leaf", "<i4")])
 SEGMENT_DT = np.dtype({
     "names": ["kernel", "d", "src", "n_groups", "group0", "ctab", "scale", "pre", "post"],
     "formats": ["<i4"] * 6 + ["<f8"] * 3,
@@ -46,7 +46,18 @@ FUNCTION_DT = np.dtype([("category", "<i4"), ("n_members", "<i4"), ("member0", "
 CATEGORY = {catalog.UNIMODAL: 0, catalog.BASIC_MULTIMODAL: 0,
             catalog.HYBRID: 1, catalog.COMPOSITION: 2}
 DISABLED = -1
-EXACT_ORDER_MAX = 128   # single-leaf pairwise sum; longer rows need the recursive tree
+EXACT_ORDER_LEAF = 128  # NumPy's pairwise-sum leaf
+EXACT_ORDER_MAX = 256   # rows up to here: <= 3 leaves, combined l0 + l1 or l0 + (l1 + l2)
+
+
+def pairwise_leaves(n: int, a: int = 0) -> list[tuple[int, int]]:
+    """The leaves [a, b) of NumPy's pairwise sum of a length-n row
+    (SURVEY.md Appendix A): n <= 128 is one leaf, else the row splits at
+    m = n/2 rounded down to a multiple of 8."""
+    if n <= EXACT_ORDER_LEAF:
+        return [(a, a + n)]
+    m = n // 2 - (n // 2) % 8
+    return pairwise_leaves(m, a) + pairwise_leaves(n - m, a + m)
 
 
 def slot_of(pos: int, n: int) -> int:
@@ -162,10 +173,24 @@ class _Builder:
         the optimum (z is then exactly post, as in the reference)."""
         m = block.shape[0]
         cols = [int(c) for c in cols]
-        order = sorted(range(m), key=lambda k: (slot_of(cols[k], n), cols[k]))
-        slots = [slot_of(cols[k], n) for k in order]
-        qb = np.searchsorted(np.asarray(slots), np.arange(10), side="left").astype(np.int32)
-        qb[9] = m
+        leaves = pairwise_leaves(n)
+        leaf_of = [next(i for i, (a, b) in enumerate(leaves) if a <= c < b) for c in cols]
+
+        def key(k):                      # (leaf, slot inside the leaf, position)
+            a, b = leaves[leaf_of[k]]
+            return (leaf_of[k], slot_of(cols[k] - a, b - a), cols[k])
+        order = sorted(range(m), key=key)
+        # per leaf: slot s spans q in [qb[s], qb[s+1]) (s < 8), tail [qb[8], qb[9])
+        leaf_qb = []
+        q0 = 0
+        for li, (a, b) in enumerate(leaves):
+            ks = [k for k in order if leaf_of[k] == li]
+            slots = [slot_of(cols[k] - a, b - a) for k in ks]
+            qb_l = q0 + np.searchsorted(np.asarray(slots, dtype=np.int64), np.arange(10), side="left")
+            qb_l[9] = q0 + len(ks)
+            leaf_qb.append(qb_l.astype(np.int32))
+            q0 += len(ks)
+        qb = leaf_qb[0] if len(leaves) == 1 else np.zeros(10, np.int32)
         mat = np.ascontiguousarray(block[:, order].T)          # mat[q, r] = block[r, order[q]]
         m4, nt, nk = (m + 3) // 4 * 4, (m + 7) // 8, (m + 3) // 4
         padded = np.zeros((nk * 4, nt * 8))
@@ -179,6 +204,10 @@ class _Builder:
         cz = -np.longdouble(pre) * mat.astype(np.longdouble).sum(axis=0) - np.longdouble(post)
         rec["cz"] = self.values(cz.astype(np.float64))
         rec["frag"] = rec["col64"] = -1                  # member(): needs the x columns
+        # float32 rows longer than a pairwise leaf: leaf table [n_leaf, qb of
+        # each leaf (10 ints)] in the index table; -1 = one leaf (qb above)
+        rec["leaf"] = (-1 if len(leaves) == 1 else
+                       self.ints(np.concatenate([[len(leaves)], *leaf_qb]).astype(np.int32)))
         self.groups.append(rec)
         self.group_src.append((block, cols, scale))
         return len(self.groups) - 1

@@ -11,40 +11,56 @@ from paper_1407_7737_b200 import catalog, instances, pack as P
 F32 = np.float32
 
 
+def _leaf_sum(v, cols, mat, qb, r):
+    t0 = t1 = t2 = F32(0)
+    for s in range(8):
+        acc = F32(0)
+        for q in range(qb[s], qb[s + 1]):
+            acc = F32(acc + F32(v[cols[q]] * mat[q, r]))
+        if s == 0:
+            t0 = acc
+        elif s == 1:
+            t0 = F32(t0 + acc)
+        elif s in (2, 4):
+            t1 = acc
+        elif s == 3:
+            t1 = F32(t1 + acc)
+            t0 = F32(t0 + t1)
+        elif s == 5:
+            t1 = F32(t1 + acc)
+        elif s == 6:
+            t2 = acc
+        else:
+            t2 = F32(t2 + acc)
+            t1 = F32(t1 + t2)
+            t0 = F32(t0 + t1)
+    for q in range(qb[8], qb[9]):
+        t0 = F32(t0 + F32(v[cols[q]] * mat[q, r]))
+    return t0
+
+
 def exact_order_rotate(pk, group, v):
     m = int(group["m"])
-    qb = group["qb"]
     cols = pk.index[group["col"]:group["col"] + m]
     rows = pk.index[group["row"]:group["row"] + m]
     m4 = (m + 3) // 4 * 4                      # rows 4-padded (float4 loads)
     mat = pk.values_f32[group["mat"]:group["mat"] + m * m4].reshape(m, m4)
+    leaf = int(group["leaf"])
+    if leaf < 0:
+        qbs = [group["qb"]]
+    else:                                      # [n_leaf, qb of each leaf]
+        nl = int(pk.index[leaf])
+        qbs = [pk.index[leaf + 1 + 10 * i:leaf + 11 + 10 * i] for i in range(nl)]
     out = {}
     for r in range(m):
-        t0 = t1 = t2 = F32(0)
-        for s in range(8):
-            acc = F32(0)
-            for q in range(qb[s], qb[s + 1]):
-                acc = F32(acc + F32(v[cols[q]] * mat[q, r]))
-            if s == 0:
-                t0 = acc
-            elif s == 1:
-                t0 = F32(t0 + acc)
-            elif s in (2, 4):
-                t1 = acc
-            elif s == 3:
-                t1 = F32(t1 + acc)
-                t0 = F32(t0 + t1)
-            elif s == 5:
-                t1 = F32(t1 + acc)
-            elif s == 6:
-                t2 = acc
-            else:
-                t2 = F32(t2 + acc)
-                t1 = F32(t1 + t2)
-                t0 = F32(t0 + t1)
-        for q in range(qb[8], qb[9]):
-            t0 = F32(t0 + F32(v[cols[q]] * mat[q, r]))
-        out[int(rows[r])] = t0
+        s = [_leaf_sum(v, cols, mat, qb, r) for qb in qbs]
+        if len(s) == 1:
+            z = s[0]
+        elif len(s) == 2:
+            z = F32(s[0] + s[1])
+        else:
+            z = F32(s[0] + F32(s[1] + s[2]))
+        out[int(rows[r])] = z
     return out
 
 
@@ -58,7 +74,7 @@ def dense_for(fn, dim, seed):
     return m.rotation.dense() if m.rotation is not None else m.hybrid.chunk_rotations[0]
 
 
-@pytest.mark.parametrize("dim", [2, 5, 8, 9, 10, 13, 30, 50, 100, 128])
+@pytest.mark.parametrize("dim", [2, 5, 8, 9, 10, 13, 30, 50, 100, 128, 129, 200, 250])
 def test_exact_order_schedule_reproduces_numpy(dim):
     disabled = frozenset(range(23, 37)) if dim < 10 else frozenset()
     pk = P.Pack(dim, 1, disabled)
@@ -173,6 +189,16 @@ def test_kernel_constants_follow_numpy():
     assert c.dtype == np.float32
     e = P.kernel_constants("elliptic", 7, np.float64)
     assert e[0] == 1.0 and e[-1] == 1e6
+
+
+def test_pairwise_leaves():
+    assert P.pairwise_leaves(100) == [(0, 100)]
+    assert P.pairwise_leaves(200) == [(0, 96), (96, 200)]
+    assert P.pairwise_leaves(250) == [(0, 120), (120, 184), (184, 250)]
+    assert P.pairwise_leaves(256) == [(0, 128), (128, 256)]
+    for n in range(129, 257):                  # the device handles 2 or 3 leaves
+        lv = P.pairwise_leaves(n)
+        assert 2 <= len(lv) <= 3 and lv[0][1] - lv[0][0] <= 128
 
 
 def test_slot_of():
