@@ -239,6 +239,7 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
   a.nbuf = L.nbuf;
   a.l2pf = l2_prefetch();
+  a.neg_zero = -0.0f;
   a.opt_rows = L.opt_rows;
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);

@@ -82,6 +82,7 @@ struct Args {
   int nbuf;         // 2: prefetch the next tile while computing this one
   int l2pf;         // 1: also pull the tile after the next in-flight one into L2
   int opt_rows;     // member optima staged in shared memory (compositions)
+  float neg_zero;   // -0.0f, opaque to ptxas (see f32_leaf)
 };
 
 struct PlanHead {
@@ -494,21 +495,28 @@ __device__ inline uint32_t gather_v(const Args<float>& a, const Smem<float>& s, 
 
 // One pairwise leaf of the float32 exact-order rotate for RR block rows and
 // the 4 points of a float4 V column: slot s walks q in [qb[s], qb[s+1]) with
-// FMUL + FADD (NumPy's r[s] += a[i] per slot), the 8 slots fold as
-// ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)) and the tail adds in order
-// (SURVEY.md Appendix A).  bp: B row qb[0] (rows r0.., stride m4).
+// a rounded product and a rounded add (NumPy's r[s] += a[i] per slot), the
+// 8 slots fold as ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)) and the tail adds in
+// order.  bp: B row qb[0] (rows r0.., stride m4).
+//
+// Packed FP32 (sm_100 FFMA2/FADD2): a pair of rows per register pair, the
+// point's v broadcast.  The product is fma(v, b, -0) -- bit-identical to
+// the rounded product -- with -0 taken from the kernel arguments: ptxas
+// contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 (12.9, even with
+// --fmad=false), which it cannot do to an fma with an unknown addend.
 template <int RR>
 __device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int bstride,
-                                         const int (&qb)[10], float (&t0)[4][RR]) {
+                                         const int (&qb)[10], float nz, float (&t0)[4][RR]) {
   constexpr int vstride = TP / 4;
-  float t1[4][RR], t2[4][RR], acc[4][RR];
-  auto load_b = [&](const float* b, float (&bb)[RR]) {
+  constexpr int RP = RR / 2;                     // row pairs
+  const float2 Z = make_float2(nz, nz);
+  float2 u0[4][RP], u1[4][RP], u2[4][RP], acc[4][RP];
+  auto load_b = [&](const float* b, float2 (&bb)[RP]) {
     if constexpr (RR == 4) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(b));
-      bb[0] = v.x; bb[1] = v.y; bb[2] = v.z; bb[3] = v.w;
+      bb[0] = make_float2(v.x, v.y); bb[1] = make_float2(v.z, v.w);
     } else {
-      const float2 v = __ldg(reinterpret_cast<const float2*>(b));
-      bb[0] = v.x; bb[1] = v.y;
+      bb[0] = __ldg(reinterpret_cast<const float2*>(b));
     }
   };
 #pragma unroll
@@ -516,48 +524,57 @@ __device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int 
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < RR; ++j) acc[i][j] = 0.0f;
+      for (int j = 0; j < RP; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
 #pragma unroll 2
     for (int q = qb[sl]; q < qb[sl + 1]; ++q, bp += bstride) {
       const float4 v = Vq[q * vstride];
-      float bb[RR];
+      float2 bb[RP];
       load_b(bp, bb);
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < RR; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(vv[i], bb[j]));
+        for (int j = 0; j < RP; ++j)
+          acc[i][j] = __fadd2_rn(acc[i][j], __ffma2_rn(make_float2(vv[i], vv[i]), bb[j], Z));
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < RR; ++j) {
-        const float x = acc[i][j];
+      for (int j = 0; j < RP; ++j) {
+        const float2 x = acc[i][j];
         switch (sl) {
-          case 0: t0[i][j] = x; break;
-          case 1: t0[i][j] = __fadd_rn(t0[i][j], x); break;
-          case 2: t1[i][j] = x; break;
-          case 3: t1[i][j] = __fadd_rn(t1[i][j], x); t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]); break;
-          case 4: t1[i][j] = x; break;
-          case 5: t1[i][j] = __fadd_rn(t1[i][j], x); break;
-          case 6: t2[i][j] = x; break;
+          case 0: u0[i][j] = x; break;
+          case 1: u0[i][j] = __fadd2_rn(u0[i][j], x); break;
+          case 2: u1[i][j] = x; break;
+          case 3: u1[i][j] = __fadd2_rn(u1[i][j], x); u0[i][j] = __fadd2_rn(u0[i][j], u1[i][j]); break;
+          case 4: u1[i][j] = x; break;
+          case 5: u1[i][j] = __fadd2_rn(u1[i][j], x); break;
+          case 6: u2[i][j] = x; break;
           default:
-            t2[i][j] = __fadd_rn(t2[i][j], x);
-            t1[i][j] = __fadd_rn(t1[i][j], t2[i][j]);
-            t0[i][j] = __fadd_rn(t0[i][j], t1[i][j]);
+            u2[i][j] = __fadd2_rn(u2[i][j], x);
+            u1[i][j] = __fadd2_rn(u1[i][j], u2[i][j]);
+            u0[i][j] = __fadd2_rn(u0[i][j], u1[i][j]);
         }
       }
   }
   for (int q = qb[8]; q < qb[9]; ++q, bp += bstride) {
     const float4 v = Vq[q * vstride];
     const float vv[4] = {v.x, v.y, v.z, v.w};
-    float bb[RR];
+    float2 bb[RP];
     load_b(bp, bb);
 #pragma unroll
-    for (int j = 0; j < RR; ++j)
+    for (int j = 0; j < RP; ++j)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) t0[i][j] = __fadd_rn(t0[i][j], __fmul_rn(vv[i], bb[j]));
+      for (int i = 0; i < 4; ++i)
+        u0[i][j] = __fadd2_rn(u0[i][j], __ffma2_rn(make_float2(vv[i], vv[i]), bb[j], Z));
   }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+      t0[i][2 * j] = u0[i][j].x;
+      t0[i][2 * j + 1] = u0[i][j].y;
+    }
 }
 
 // the V tile is in place (gather_v + barrier)
@@ -596,7 +613,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
         const int r0 = rq * 4 + pass * RR;
         if (r0 >= m) break;
         float z[4][RR];
-        f32_leaf<RR>(Vq, a.values + G.mat + r0, m4, qb, z);
+        f32_leaf<RR>(Vq, a.values + G.mat + r0, m4, qb, a.neg_zero, z);
 #pragma unroll
         for (int j = 0; j < RR; ++j) {
           if (r0 + j >= m) break;
@@ -620,15 +637,15 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
         int qb[10];
 #pragma unroll
         for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 1 + k);
-        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, z);
+        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, z);
 #pragma unroll
         for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 11 + k);
-        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, u);
+        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, u);
         if (nl == 3) {
           float w[4][RR];
 #pragma unroll
           for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 21 + k);
-          f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, w);
+          f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, w);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
