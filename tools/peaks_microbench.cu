@@ -41,6 +41,35 @@ __global__ void k_fmuladd(float* out, int iters, float a, float b) {
   float s = 0; for (int i = 0; i < ILP; ++i) s += acc[i];
   if (s == 12345.678f) out[0] = s;
 }
+// packed FP32 (sm_100 FFMA2 / FADD2), the exact-order rotate's instruction
+// pair: product as fma(a, b, -0) with an opaque -0, then a separate add
+template<int ILP>
+__global__ void k_ffma2(float* out, int iters, float a, float b) {
+  float2 acc[ILP];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) acc[i] = make_float2(threadIdx.x * 1e-3f + i, i);
+  const float2 A = make_float2(a, a), B = make_float2(b, b);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) acc[i] = __ffma2_rn(acc[i], A, B);
+  }
+  float s = 0; for (int i = 0; i < ILP; ++i) s += acc[i].x + acc[i].y;
+  if (s == 12345.678f) out[0] = s;
+}
+template<int ILP>
+__global__ void k_fmul2_fadd2(float* out, int iters, float a, float nz) {
+  float2 acc[ILP];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) acc[i] = make_float2(threadIdx.x * 1e-3f + i, i);
+  const float2 Z = make_float2(nz, nz);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i)
+      acc[i] = __fadd2_rn(acc[i], __ffma2_rn(acc[i], make_float2(a, a), Z));
+  }
+  float s = 0; for (int i = 0; i < ILP; ++i) s += acc[i].x + acc[i].y;
+  if (s == 12345.678f) out[0] = s;
+}
 template<int ILP>
 __global__ void k_dmma_k4(double* out, int iters) {
   double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, b0 = 0.5;
@@ -110,6 +139,10 @@ int main() {
   printf(", \"ffma_tflops\": %.2f", nthr * iters * 8 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&]{ k_fmuladd<8><<<blocks, threads>>>((float*)dout, iters, 1.0000001f, 1e-9f); });
   printf(", \"fmul_fadd_tflops\": %.2f", nthr * iters * 8 * 2 / (ms * 1e-3) / 1e12);
+  ms = timeit([&]{ k_ffma2<8><<<blocks, threads>>>((float*)dout, iters, 1.0000001f, 1e-9f); });
+  printf(", \"ffma2_tflops\": %.2f", nthr * iters * 8 * 4 / (ms * 1e-3) / 1e12);
+  ms = timeit([&]{ k_fmul2_fadd2<8><<<blocks, threads>>>((float*)dout, iters, 1.0000001f, -0.0f); });
+  printf(", \"fmul2_fadd2_tflops\": %.2f", nthr * iters * 8 * 4 / (ms * 1e-3) / 1e12);
   ms = timeit([&]{ k_dmma_k4<4><<<blocks, threads>>>(dout, iters / 4); });
   printf(", \"dmma_m16n8k4_tflops\": %.2f", nthr / 32 * (iters / 4) * 4 * 16 * 8 * 4 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&]{ k_dmma_k16<4><<<blocks, threads>>>(dout, iters / 16); });
