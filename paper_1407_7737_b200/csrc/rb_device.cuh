@@ -462,7 +462,13 @@ __device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, 
 // ------------------------------------------------------------ rotate fp32
 // Exact NumPy order (transforms.py:42-48): rounded products, per-slot
 // accumulation in q-order, slot fold ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)),
-// ordered tail.  VS is [q][TP]; B rows are 4-padded (one float4 per q).
+// ordered tail.  VS is [q][TP] with point p at word vslot(p); B rows are
+// 4-padded (one float4 per q).  A rotate item owns points pq + 8i (i < 4),
+// one float4 of V: the 8 items of a warp's z store then cover 4 residues of
+// p mod 4, i.e. 4 distinct banks at ldz = 8 (mod 32) (2-way instead of 8-way
+// conflicts; the pack orders block rows so the warp's 4 rows differ mod 8).
+__device__ __forceinline__ int vslot(int p) { return (p & 7) * 4 + (p >> 3); }
+
 // gather: V[vq + q][p] = scale*(x[p][src_q] - o_q) + pre   (engine.py:97-100)
 // for the groups of plan segments [s_first, s_end).  Every x of the tile is
 // read here once per member, so it also returns the max |x| bit pattern over
@@ -480,13 +486,14 @@ __device__ inline uint32_t gather_v(const Args<float>& a, const Smem<float>& s, 
     const int kp = round4(P.grp[g0 + g].m);
     const int* qs = s.qsrc + P.gq0[g0 + g];
     const float* qo = s.qo + P.gq0[g0 + g];
+#pragma unroll 4
     for (int e = threadIdx.x; e < TP * kp; e += NT) {
       const int q = e / TP, p = e - q * TP;
       const float x = s.XS[p * a.dim + qs[q]];
       if (p < nv) mx = max(mx, __float_as_uint(x) & 0x7fffffffu);
       float v = scale * (x - qo[q]);
       if (pre != 0.0f) v = v + pre;
-      s.VS[(vq + q) * TP + p] = v;
+      s.VS[(vq + q) * TP + vslot(p)] = v;
     }
     vq += kp;
   }
@@ -620,7 +627,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
           const int row = prow[r0 + j];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            put_z<CHECK>(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(z[i][j], post) : z[i][j], nf);
+            put_z<CHECK>(a, s, pq + 8 * i, row, post != 0.0f ? __fadd_rn(z[i][j], post) : z[i][j], nf);
         }
       }
     } else {
@@ -658,7 +665,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float zz = __fadd_rn(z[i][j], u[i][j]);
-            put_z<CHECK>(a, s, pq * 4 + i, row, post != 0.0f ? __fadd_rn(zz, post) : zz, nf);
+            put_z<CHECK>(a, s, pq + 8 * i, row, post != 0.0f ? __fadd_rn(zz, post) : zz, nf);
           }
         }
       }

@@ -60,6 +60,27 @@ def pairwise_leaves(n: int, a: int = 0) -> list[tuple[int, int]]:
     return pairwise_leaves(m, a) + pairwise_leaves(n - m, a + m)
 
 
+def store_row_order(pos) -> list[int]:
+    """Order of a block's rows for the float32 rotate's z stores: row r is
+    computed by item row-quad r // 4 (element r % 4), and a warp stores the
+    same element of 4 consecutive row-quads at once (rb_device.cuh, rotate
+    float), so rows 4 rq + j, 4 (rq+1) + j, ... should differ in position
+    mod 8 (distinct shared-memory banks at ldz = 8 mod 32).  Greedy: avoid
+    the residues of the previous 3 row-quads' row j, prefer (rq + 2j) mod 8."""
+    pos = [int(p) for p in pos]
+    remaining = list(range(len(pos)))
+    out: list[int] = []
+    for r in range(len(pos)):
+        rq, j = divmod(r, 4)
+        taken = {pos[out[4 * (rq - k) + j]] % 8 for k in (1, 2, 3) if rq - k >= 0}
+        want = (rq + 2 * j) % 8
+        cands = [i for i in remaining if pos[i] % 8 not in taken] or remaining
+        pick = min(cands, key=lambda i: ((pos[i] % 8 - want) % 8, pos[i]))
+        out.append(pick)
+        remaining.remove(pick)
+    return out
+
+
 def slot_of(pos: int, n: int) -> int:
     """Accumulator slot of element ``pos`` in NumPy's pairwise sum of a
     contiguous length-n row: 0..7, or 8 for the tail."""
@@ -173,6 +194,9 @@ class _Builder:
         the optimum (z is then exactly post, as in the reference)."""
         m = block.shape[0]
         cols = [int(c) for c in cols]
+        rorder = store_row_order(rows)             # row order is free: rows are independent
+        block = block[rorder]
+        rows = [int(rows[i]) for i in rorder]
         leaves = pairwise_leaves(n)
         leaf_of = [next(i for i, (a, b) in enumerate(leaves) if a <= c < b) for c in cols]
 
