@@ -52,7 +52,8 @@ typedef int32_t rb_status;
  * by the NumPy pairwise-sum accumulator slot they fall in (slot = column % 8
  * below the last multiple of 8, then the ordered tail), ascending inside a
  * slot, so exact-order single precision can replay NumPy's rounding
- * (SURVEY.md Appendix A).  The segment length must be <= 128 for that. */
+ * (SURVEY.md Appendix A).  Segments longer than 128 are NumPy's recursive
+ * split: columns sorted by (leaf, slot, index), see `leaf`; up to 256. */
 typedef struct rb_group {
   int32_t m;        /* block size */
   int32_t qb[10];   /* slot s spans q in [qb[s], qb[s+1]) for s < 8; tail [qb[8], qb[9]); qb[9] == m */

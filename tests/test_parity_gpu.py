@@ -26,7 +26,7 @@ def assert_close(got, want, prec, what=""):
     assert not bad.any(), (what, prec, np.flatnonzero(bad)[:5], got[bad][:5], want[bad][:5])
 
 
-@pytest.fixture(scope="module", params=[2, 10, 30, 50, 100, 200, 250])
+@pytest.fixture(scope="module", params=[2, 10, 30, 32, 50, 64, 96, 100, 200, 250])
 def pair(request):
     dim = request.param
     eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=4096, seed=0))
@@ -163,4 +163,38 @@ def test_large_batch_properties():
             assert_close(sub, orc.evaluate(fn, xs, prec), prec, f"large fn={fn}")
             alone = eng.evaluate(fn, xs, precision=prec).values
             assert np.array_equal(alone, sub)
+    eng.dispose()
+
+
+def test_unaligned_device_rows_take_the_per_row_copy_path():
+    # a device view whose base is not 16-byte aligned cannot use the bulk
+    # tile copy (Args.tma = 0): same values as the aligned buffer
+    import torch
+    dim, n = 30, 300
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=n, seed=5))
+    x = population(dim, n, seed=5)
+    for prec, tdt in (("double", torch.float64), ("single", torch.float32)):
+        flat = torch.empty(n * dim + 1, dtype=tdt, device="cuda")
+        flat[1:] = torch.from_numpy(x.reshape(-1)).to(tdt).cuda()
+        xu = flat[1:].view(n, dim)
+        assert xu.data_ptr() % 16 != 0
+        for fn in (0, 8, 26, 34):
+            got = eng.evaluate(fn, xu, precision=prec).values.cpu().numpy()
+            want = eng.evaluate(fn, x, precision=prec).values
+            assert np.array_equal(got, want), (fn, prec)
+    eng.dispose()
+
+
+def test_c_abi_rejects_an_empty_batch():
+    # PointBatch(np.zeros((0, 10))) is a ValueError (test_engine.py:120-124):
+    # the C ABI answers RB_E_INVALID_ARGUMENT and writes nothing
+    import ctypes
+    from paper_1407_7737_b200 import _lib
+    eng = rb.initialize(rb.EngineConfig(dim=10, max_concurrency=8, seed=1))
+    lib = _lib.load()
+    f = np.full(1, 7.0)
+    x = np.zeros((1, 10))
+    st = lib.rb_h_func_evaluate(eng._handle, 0, x.ctypes.data_as(ctypes.c_void_p), 0,
+                                f.ctypes.data_as(ctypes.c_void_p))
+    assert st == 7 and f[0] == 7.0
     eng.dispose()
