@@ -59,6 +59,7 @@ constexpr int MAX_SEGMENTS = 16;
 constexpr int MAX_GROUPS = 16;
 constexpr int MAX_UNITS = 512;  // fp64 DMMA units (m-tile x n-tile of a group) per function
 constexpr int NTC = 2;          // DMMA n-tiles (8 rows) sharing one A fragment per k-step
+                                // (3 measured: +1-3% basic, -10-18% compositions: spills)
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
 template <class T>
