@@ -352,10 +352,12 @@ def run_ours(args):
         # D2H of chunk c-1's fitness values run on a copy stream while chunk c
         # is evaluated (every function, both precisions; values land in a
         # resident results buffer through Engine.evaluate(out=...))
-        n_chunks = 8 if world == 1 and shard.count >= 8 * 4096 else 1
+        n_chunks = int(os.environ.get("RB_E2E_CHUNKS", "8"))
+        n_chunks = n_chunks if world == 1 and shard.count >= n_chunks * 4096 else 1
         bounds = [shard.count * c // n_chunks for c in range(n_chunks + 1)]
         nc_max = max(bounds[c + 1] - bounds[c] for c in range(n_chunks))
-        copy_stream = torch.cuda.Stream(device=dev)
+        copy_stream = torch.cuda.Stream(device=dev)     # H2D
+        out_stream = torch.cuda.Stream(device=dev)      # D2H (PCIe is full duplex)
         res, host_res = {}, {}
         if world == 1:                    # resident results of two chunks in flight
             res = {p: torch.empty((2, len(fns), nc_max), device=dev,
@@ -386,13 +388,14 @@ def run_ours(args):
                     for i, fn in enumerate(fns):
                         engine.evaluate(fn, xcs[p], p, out=res[p][c % 2, i, :nc])
                 ev_done[c].record(stream)
-                with torch.cuda.stream(copy_stream):
-                    copy_stream.wait_event(ev_done[c])
+                with torch.cuda.stream(out_stream):
+                    out_stream.wait_event(ev_done[c])
                     for p in precs:
                         host_res[p][c % 2, :, :nc].copy_(res[p][c % 2, :, :nc], non_blocking=True)
                         d2h += len(fns) * nc * res[p].element_size()
-                    ev_out[c].record(copy_stream)
+                    ev_out[c].record(out_stream)
             stream.wait_stream(copy_stream)
+            stream.wait_stream(out_stream)
             torch.cuda.synchronize()
 
         e2e_step = e2e_step_pipelined if world == 1 else e2e_step_plain
@@ -414,8 +417,8 @@ def run_ours(args):
             ems = float(tt.item())
         e2e = {"value": evals / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
-               "pipeline": (f"{n_chunks} row chunks: H2D of X and D2H of every fitness vector on a "
-                            "copy stream, overlapped with evaluation" if world == 1 else
+               "pipeline": (f"{n_chunks} row chunks: H2D of X and D2H of every fitness vector on two "
+                            "copy streams, overlapped with evaluation" if world == 1 else
                             "H2D, evaluate + NCCL all-gather, D2H per function")}
         del host_x, host_f, host_res, res
 
