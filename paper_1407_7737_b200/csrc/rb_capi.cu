@@ -162,8 +162,8 @@ struct rb_engine {
   int32_t* d_index = nullptr;
   double* d_v64 = nullptr;
   float* d_v32 = nullptr;
-  int* d_flags = nullptr;                    // ring of per-call non-finite flags
-  int* h_flags = nullptr;                    // pinned mirror
+  int* h_flags = nullptr;                    // ring of per-call non-finite flags, mapped
+  int* d_flags = nullptr;                    // pinned host memory (device alias of h_flags)
   std::atomic<int> next_flag{0};
   std::mutex host_mu;                        // host-pointer API staging buffers
   void* stage_x = nullptr;
@@ -186,7 +186,6 @@ void release(rb_engine* e) {
   cudaFree(e->d_index);
   cudaFree(e->d_v64);
   cudaFree(e->d_v32);
-  cudaFree(e->d_flags);
   cudaFree(e->stage_x);
   cudaFree(e->stage_f);
   if (e->h_flags) cudaFreeHost(e->h_flags);
@@ -217,8 +216,13 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   RB_CUDA(cudaGetDevice(&prev));
   if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
   const int slot = e->next_flag.fetch_add(1) % kFlagSlots;
+  // the flag lives in mapped pinned memory: cleared by the host, set by the
+  // kernel with a plain store over PCIe, read after the stream sync (no
+  // memset / D2H copy that would queue behind bulk transfers on the copy
+  // engines)
+  volatile int* hflag = e->h_flags + slot;
+  *hflag = 0;
   int* dflag = e->d_flags + slot;
-  RB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), stream));
 
   rb::Args<T> a;
   a.x = x;
@@ -246,9 +250,8 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   void* args[] = {&a};
   RB_CUDA(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream));
   g_launches.fetch_add(1);
-  RB_CUDA(cudaMemcpyAsync(e->h_flags + slot, dflag, sizeof(int), cudaMemcpyDeviceToHost, stream));
   RB_CUDA(cudaStreamSynchronize(stream));
-  const int flag = e->h_flags[slot];
+  const int flag = *hflag;
   if (prev != e->device) cudaSetDevice(prev);
   if (flag) return fail(RB_E_NON_FINITE_INPUT, "batch contains NaN or infinity (kernel input not finite)");
   return RB_OK;
@@ -482,10 +485,12 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   if (s == RB_OK) s = upload(&e->d_index, pk->index, pk->n_index);
   if (s == RB_OK) s = upload(&e->d_v64, pk->values_f64, pk->n_values);
   if (s == RB_OK) s = upload(&e->d_v32, pk->values_f32, pk->n_values);
-  if (s == RB_OK && cudaMalloc(&e->d_flags, sizeof(int) * kFlagSlots) != cudaSuccess)
-    s = fail(RB_E_CUDA, "flag allocation failed");
-  if (s == RB_OK && cudaMallocHost(&e->h_flags, sizeof(int) * kFlagSlots) != cudaSuccess)
-    s = fail(RB_E_CUDA, "pinned flag allocation failed");
+  if (s == RB_OK && cudaHostAlloc(reinterpret_cast<void**>(&e->h_flags), sizeof(int) * kFlagSlots,
+                                   cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    s = fail(RB_E_CUDA, "mapped flag allocation failed");
+  if (s == RB_OK && cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_flags), e->h_flags, 0) !=
+                        cudaSuccess)
+    s = fail(RB_E_CUDA, "mapped flag pointer failed");
   if (s == RB_OK && cudaStreamCreateWithFlags(&e->host_stream, cudaStreamNonBlocking) != cudaSuccess)
     s = fail(RB_E_CUDA, "stream creation failed");
   cudaSetDevice(prev);

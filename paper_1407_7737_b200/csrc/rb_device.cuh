@@ -75,7 +75,7 @@ struct Args {
   const int32_t* index;
   const T* values;
   int fn;
-  int* flag;        // set to 2 when a kernel input is not finite
+  int* flag;        // set to 2 when a kernel input is not finite (mapped host memory)
   int ldz;          // ZS row stride (elements)
   int ldv;          // fp32 V tile rows (sum of 4-padded group sizes)
   int max_q;        // capacity of the plan's per-column tables
@@ -85,6 +85,13 @@ struct Args {
   int opt_rows;     // member optima staged in shared memory (compositions)
   float neg_zero;   // -0.0f, opaque to ptxas (see f32_leaf)
 };
+
+// every writer stores the same value: a plain store (the flag is in mapped
+// host memory, where device atomics need not be supported)
+template <class T>
+__device__ __forceinline__ void raise_flag(const Args<T>& a) {
+  *reinterpret_cast<volatile int*>(a.flag) = 2;
+}
 
 struct PlanHead {
   rb_function fn;
@@ -747,7 +754,7 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
     if constexpr (sizeof(T) == 4) {
       const uint32_t mx = gather_v(a, s, s_first, s_end, t.scanned ? 0 : t.nv);
       if (!t.scanned) {                    // X scan of this tile (see evaluate_kernel)
-        if (mx >= 0x7f800000u) atomicOr(a.flag, 2);
+        if (mx >= 0x7f800000u) raise_flag(a);
         t.check_z = __syncthreads_or(mx >= 0x71800000u) != 0;
         t.scanned = true;
       } else {
@@ -756,7 +763,7 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
     }
     nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
   }
-  if (nf & t.live) atomicOr(a.flag, 2);
+  if (nf & t.live) raise_flag(a);
   __syncthreads();
   return s.ZS;
 }
@@ -1005,7 +1012,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
         for (int j = l8; j < a.dim; j += 8) mx = max(mx, xw[j * W + W - 1] & 0x7fffffffu);
       }
       const bool big = sizeof(T) == 8 ? mx >= 0x7bf00000u : mx >= 0x71800000u;   // x_large
-      if (sizeof(T) == 8 ? mx >= 0x7ff00000u : mx >= 0x7f800000u) atomicOr(a.flag, 2);
+      if (sizeof(T) == 8 ? mx >= 0x7ff00000u : mx >= 0x7f800000u) raise_flag(a);
       t.check_z = __syncthreads_or(big) != 0;
     }
     RB_PHASE_MARK(c_loaded);
