@@ -536,12 +536,27 @@ __device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int 
   };
 #pragma unroll
   for (int sl = 0; sl < 8; ++sl) {
+    // a slot starts from its first product (NumPy's r[k] = a[k]), not 0 + a[k]
+    int q = qb[sl];
+    if (q < qb[sl + 1]) {
+      const float4 v = Vq[q * vstride];
+      float2 bb[RP];
+      load_b(bp, bb);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < RP; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
+        for (int j = 0; j < RP; ++j) acc[i][j] = __ffma2_rn(make_float2(vv[i], vv[i]), bb[j], Z);
+      ++q;
+      bp += bstride;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < RP; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
+    }
 #pragma unroll 2
-    for (int q = qb[sl]; q < qb[sl + 1]; ++q, bp += bstride) {
+    for (; q < qb[sl + 1]; ++q, bp += bstride) {
       const float4 v = Vq[q * vstride];
       float2 bb[RP];
       load_b(bp, bb);
