@@ -31,6 +31,10 @@
 #ifndef RB_MIN_BLOCKS_F32
 #define RB_MIN_BLOCKS_F32 2
 #endif
+#ifndef RB_F32_UNROLL
+#define RB_F32_UNROLL 2           // column-loop unroll of the float32 rotate slots
+#endif
+constexpr int kF32Unroll = RB_F32_UNROLL;
 #ifndef RB_F32_ROWS
 #define RB_F32_ROWS 4             // rows per pass of the float32 rotate tile (4 or 2)
 #endif
@@ -555,7 +559,7 @@ __device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int 
 #pragma unroll
         for (int j = 0; j < RP; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
     }
-#pragma unroll 2
+#pragma unroll kF32Unroll
     for (; q < qb[sl + 1]; ++q, bp += bstride) {
       const float4 v = Vq[q * vstride];
       float2 bb[RP];
