@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <atomic>
 #include <cstdint>
 #include <mutex>
@@ -168,6 +169,7 @@ struct rb_engine {
   std::mutex host_mu;                        // host-pointer API staging buffers
   void* stage_x = nullptr;
   void* stage_f = nullptr;
+  void* pin_x = nullptr;                     // pinned staging of small host batches (x, then f)
   size_t stage_bytes_x = 0, stage_bytes_f = 0;
   cudaStream_t host_stream = nullptr;
 };
@@ -188,15 +190,18 @@ void release(rb_engine* e) {
   cudaFree(e->d_v32);
   cudaFree(e->stage_x);
   cudaFree(e->stage_f);
+  if (e->pin_x) cudaFreeHost(e->pin_x);
   if (e->h_flags) cudaFreeHost(e->h_flags);
   if (e->host_stream) cudaStreamDestroy(e->host_stream);
   cudaSetDevice(prev);
   delete e;
 }
 
+// Validation in the reference's order, then the launch on `stream`; the
+// caller has made e->device current, synchronises and reads *flag_out.
 template <class T>
-rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
-                          cudaStream_t stream) {
+rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
+                      cudaStream_t stream, volatile int** flag_out) {
   // validation in the reference's order (engine.py:180-203)
   if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
   if (fn_id < 0 || fn_id >= (int32_t)e->fns.size())
@@ -212,9 +217,6 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
     return fail(RB_E_UNSUPPORTED, "single precision needs rotation blocks of length <= 256");
   const Launch& L = e->launch[pi][fn_id];
 
-  int prev = 0;
-  RB_CUDA(cudaGetDevice(&prev));
-  if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
   const int slot = e->next_flag.fetch_add(1) % kFlagSlots;
   // the flag lives in mapped pinned memory: cleared by the host, set by the
   // kernel with a plain store over PCIe, read after the stream sync (no
@@ -250,23 +252,40 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   void* args[] = {&a};
   RB_CUDA(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream));
   g_launches.fetch_add(1);
-  RB_CUDA(cudaStreamSynchronize(stream));
-  const int flag = *hflag;
-  if (prev != e->device) cudaSetDevice(prev);
-  if (flag) return fail(RB_E_NON_FINITE_INPUT, "batch contains NaN or infinity (kernel input not finite)");
+  *flag_out = hflag;
   return RB_OK;
 }
 
+rb_status non_finite() {
+  return fail(RB_E_NON_FINITE_INPUT, "batch contains NaN or infinity (kernel input not finite)");
+}
+
 template <class T>
-rb_status evaluate_host(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
+rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
+                          cudaStream_t stream) {
   if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
-  if (n < 1 || n > e->max_concurrency || !x || !f || fn_id < 0 ||
-      fn_id >= (int32_t)e->fns.size() || e->fns[fn_id].category == RB_DISABLED)
-    return evaluate_device<T>(e, fn_id, x, n, f, nullptr);   // reports the error
-  std::lock_guard<std::mutex> lock(e->host_mu);
   int prev = 0;
   RB_CUDA(cudaGetDevice(&prev));
-  RB_CUDA(cudaSetDevice(e->device));
+  if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
+  volatile int* flag = nullptr;
+  rb_status s = launch_eval<T>(e, fn_id, x, n, f, stream, &flag);
+  if (s == RB_OK) {
+    const cudaError_t err = cudaStreamSynchronize(stream);
+    if (err != cudaSuccess) s = fail(RB_E_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(err));
+    else if (*flag) s = non_finite();
+  }
+  if (prev != e->device) cudaSetDevice(prev);
+  return s;
+}
+
+// Host-pointer call (device current, host_mu held): one H2D, the launch,
+// one D2H and a single synchronisation.  Batches up to kPinnedStage bytes
+// go through pinned staging buffers (fast async copies, f written only on
+// success); larger ones copy from / to the caller's pageable memory.
+constexpr size_t kPinnedStage = size_t(8) << 20;
+
+template <class T>
+rb_status evaluate_host_locked(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
   const size_t bx = sizeof(T) * (size_t)n * e->dim, bf = sizeof(T) * (size_t)n;
   if (bx > e->stage_bytes_x) {
     cudaFree(e->stage_x);
@@ -280,11 +299,42 @@ rb_status evaluate_host(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f
     RB_CUDA(cudaMalloc(&e->stage_f, bf));
     e->stage_bytes_f = bf;
   }
-  RB_CUDA(cudaMemcpyAsync(e->stage_x, x, bx, cudaMemcpyHostToDevice, e->host_stream));
-  const rb_status s = evaluate_device<T>(e, fn_id, static_cast<const T*>(e->stage_x), n,
-                                         static_cast<T*>(e->stage_f), e->host_stream);
-  if (s == RB_OK) RB_CUDA(cudaMemcpyAsync(f, e->stage_f, bf, cudaMemcpyDeviceToHost, e->host_stream));
+  const size_t fo = (bx + 255) & ~size_t(255);       // f's offset in the pinned buffer
+  const bool pinned = fo + bf <= kPinnedStage;
+  if (pinned && !e->pin_x) RB_CUDA(cudaMallocHost(&e->pin_x, kPinnedStage));
+  const void* src = x;
+  void* dst = f;
+  if (pinned) {
+    std::memcpy(e->pin_x, x, bx);
+    src = e->pin_x;
+    dst = static_cast<unsigned char*>(e->pin_x) + fo;
+  }
+  RB_CUDA(cudaMemcpyAsync(e->stage_x, src, bx, cudaMemcpyHostToDevice, e->host_stream));
+  volatile int* flag = nullptr;
+  rb_status s = launch_eval<T>(e, fn_id, static_cast<const T*>(e->stage_x), n,
+                               static_cast<T*>(e->stage_f), e->host_stream, &flag);
+  if (s != RB_OK) {
+    cudaStreamSynchronize(e->host_stream);
+    return s;
+  }
+  RB_CUDA(cudaMemcpyAsync(dst, e->stage_f, bf, cudaMemcpyDeviceToHost, e->host_stream));
   RB_CUDA(cudaStreamSynchronize(e->host_stream));
+  if (*flag) return non_finite();
+  if (pinned) std::memcpy(f, dst, bf);
+  return RB_OK;
+}
+
+template <class T>
+rb_status evaluate_host(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (n < 1 || n > e->max_concurrency || !x || !f || fn_id < 0 ||
+      fn_id >= (int32_t)e->fns.size() || e->fns[fn_id].category == RB_DISABLED)
+    return evaluate_device<T>(e, fn_id, x, n, f, nullptr);   // reports the error
+  std::lock_guard<std::mutex> lock(e->host_mu);
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  RB_CUDA(cudaSetDevice(e->device));
+  const rb_status s = evaluate_host_locked<T>(e, fn_id, x, n, f);
   cudaSetDevice(prev);
   return s;
 }
