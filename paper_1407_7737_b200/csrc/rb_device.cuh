@@ -637,7 +637,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
     const int* prow = s.prow + P.gq0[g];
     // column q: V row vq + q (4 points, one float4) and B row q
     const float4* Vq = reinterpret_cast<const float4*>(s.VS + vq * TP + pq * 4);
-    if (G.leaf < 0) {                          // one pairwise leaf (m <= 128)
+    if (G.leaf < 0) {                          // one pairwise leaf (segment rows <= 128)
       constexpr int RR = RB_F32_ROWS;
       int qb[10];
 #pragma unroll
