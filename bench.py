@@ -67,6 +67,34 @@ def parse():
 
 
 # ----------------------------------------------------------------- helpers
+NCU_PIPES = {
+    "tensor": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "fp64": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "fma": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "xu": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "issue": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+}
+
+
+def ncu_pipes(fn, prec):
+    """Pipe utilisation (% of peak while active) of the dominant launch from
+    its latest committed ncu --set full summary (profiles/r01/v*/), or None:
+    the transcendental work the rotate-flop roofline leaves out."""
+    import glob
+    cands = sorted(glob.glob(str(ROOT / "profiles" / "r01" / "v*" / f"ncu_full_fn{fn}_{prec}.txt")),
+                   key=lambda p: int(Path(p).parent.name[1:]))
+    if not cands:
+        return None
+    vals = {}
+    for line in Path(cands[-1]).read_text().splitlines():
+        parts = line.split()
+        if len(parts) == 2:
+            vals[parts[0]] = parts[1]
+    out = {k: round(float(vals[m]), 1) for k, m in NCU_PIPES.items() if m in vals}
+    out["source"] = str(Path(cands[-1]).relative_to(ROOT))
+    return out
+
+
 def load_json(path):
     try:
         return json.loads(Path(path).read_text())
@@ -322,6 +350,7 @@ def run_ours(args):
         # utilisation in profiles/)
         "compute_pipe": ("fp64 DMMA (mma.sync m16n8k4)" if dom["precision"] == "double"
                          else "fp32 SIMT FMUL+FADD, exact NumPy order"),
+        "pipe_utilization": ncu_pipes(dom["fn"], dom["precision"]),
     }
 
     # e2e through the public API from pinned host memory
