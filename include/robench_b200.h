@@ -53,7 +53,7 @@ typedef int32_t rb_status;
  * below the last multiple of 8, then the ordered tail), ascending inside a
  * slot, so exact-order single precision can replay NumPy's rounding
  * (SURVEY.md Appendix A).  Segments longer than 128 are NumPy's recursive
- * split: columns sorted by (leaf, slot, index), see `leaf`; up to 256. */
+ * split: columns sorted by (leaf, slot, index), see `leaf`; up to 968 (4 pending sums). */
 typedef struct rb_group {
   int32_t m;        /* block size */
   int32_t qb[10];   /* slot s spans q in [qb[s], qb[s+1]) for s < 8; tail [qb[8], qb[9]); qb[9] == m */
@@ -69,9 +69,11 @@ typedef struct rb_group {
                        computes z_r = sum_q (scale B)[q][r] (x[src_q] - o[src_q]) - cz[r] */
   int32_t col64;    /* index[col64 + q]: input position of the q-th float64 column (an order
                        whose 4-column k-steps read shared memory without bank conflicts) */
-  int32_t leaf;     /* -1: one pairwise leaf (qb above).  Else index[leaf ...] = [n_leaf (2 or 3),
-                       qb of leaf 0, 1(, 2) (10 ints each, absolute q)]: float32 rows of length
-                       129..256 are summed as NumPy's tree l0 + l1 or l0 + (l1 + l2) */
+  int32_t leaf;     /* -1: one pairwise leaf (qb above).  -2: tree deeper than the device stack
+                       (float32 unsupported).  Else index[leaf ...] = [n_leaf, then per leaf
+                       its qb (10 ints, absolute q) and the number of (left + right) additions
+                       that follow it]: float32 rows longer than 128 replay NumPy's recursive
+                       pairwise tree as a post-order program (pack.py pairwise_program) */
 } rb_group;
 
 /* One kernel application: v = scale*((x - o)[src..]) + pre; z = R v + post;

@@ -214,7 +214,7 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
   if (n < 1 || !x || !f) return fail(RB_E_INVALID_ARGUMENT, "empty batch or null pointer");
   const int pi = sizeof(T) == 8 ? 0 : 1;
   if (pi == 1 && !e->exact_ok[fn_id])
-    return fail(RB_E_UNSUPPORTED, "single precision needs rotation blocks of length <= 256");
+    return fail(RB_E_UNSUPPORTED, "single precision needs rotated segments whose pairwise tree fits the device stack (any length <= 968)");
   const Launch& L = e->launch[pi][fn_id];
 
   const int slot = e->next_flag.fetch_add(1) % kFlagSlots;
@@ -374,8 +374,8 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
           max_q += rb::round8(pk->groups[g].m);
           q4 += (pk->groups[g].m + 3) & ~3;
           units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
+          if (pk->groups[g].leaf == -2) e->exact_ok[fi] = 0;   // pairwise tree too deep
         }
-        if (sg.n_groups && sg.d > 256) e->exact_ok[fi] = 0;
       }
       ldv = std::max(ldv, q4);
     }

@@ -658,8 +658,12 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
         }
       }
     } else {
-      // 129..256: NumPy's tree over 2 or 3 leaves, l0 + l1 or l0 + (l1 + l2)
+      // rows longer than 128: NumPy's pairwise tree over the leaves, run as
+      // a post-order program (pack.py pairwise_program): each leaf's sum is
+      // pushed, then the given number of (left + right) additions pop the
+      // stack.  Stack slots are registers (static indices under sp tests).
       constexpr int RR = 2;
+      constexpr int SD = 4;                    // pack.py EXACT_ORDER_STACK
       const int* L = a.index + G.leaf;
       const int nl = __ldg(L);
 #pragma unroll 1
@@ -667,23 +671,36 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
         const int r0 = rq * 4 + pass * RR;
         if (r0 >= m) break;
         const float* B = a.values + G.mat + r0;
-        float z[4][RR], u[4][RR];
-        int qb[10];
+        float st[SD][4][RR];
+        int sp = 0;
+#pragma unroll 1
+        for (int lf = 0; lf < nl; ++lf) {
+          const int* E = L + 1 + 11 * lf;
+          int qb[10];
 #pragma unroll
-        for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 1 + k);
-        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, z);
+          for (int k = 0; k < 10; ++k) qb[k] = __ldg(E + k);
+          float z[4][RR];
+          f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, z);
 #pragma unroll
-        for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 11 + k);
-        f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, u);
-        if (nl == 3) {
-          float w[4][RR];
+          for (int d = 0; d < SD; ++d)
+            if (d == sp) {
 #pragma unroll
-          for (int k = 0; k < 10; ++k) qb[k] = __ldg(L + 21 + k);
-          f32_leaf<RR>(Vq, B + qb[0] * m4, m4, qb, a.neg_zero, w);
+              for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+                for (int j = 0; j < RR; ++j) st[d][i][j] = z[i][j];
+            }
+          ++sp;
+          for (int c = __ldg(E + 10); c > 0; --c) {
 #pragma unroll
-            for (int j = 0; j < RR; ++j) u[i][j] = __fadd_rn(u[i][j], w[i][j]);
+            for (int d = 1; d < SD; ++d)
+              if (d == sp - 1) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                  for (int j = 0; j < RR; ++j) st[d - 1][i][j] = __fadd_rn(st[d - 1][i][j], st[d][i][j]);
+              }
+            --sp;
+          }
         }
 #pragma unroll
         for (int j = 0; j < RR; ++j) {
@@ -691,7 +708,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
           const int row = prow[r0 + j];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float zz = __fadd_rn(z[i][j], u[i][j]);
+            const float zz = st[0][i][j];
             put_z<CHECK>(a, s, pq + 8 * i, row, post != 0.0f ? __fadd_rn(zz, post) : zz, nf);
           }
         }

@@ -47,7 +47,7 @@ CATEGORY = {catalog.UNIMODAL: 0, catalog.BASIC_MULTIMODAL: 0,
             catalog.HYBRID: 1, catalog.COMPOSITION: 2}
 DISABLED = -1
 EXACT_ORDER_LEAF = 128  # NumPy's pairwise-sum leaf
-EXACT_ORDER_MAX = 256   # rows up to here: <= 3 leaves, combined l0 + l1 or l0 + (l1 + l2)
+EXACT_ORDER_STACK = 4   # device stack of pending subtree sums (every row length <= 968)
 
 
 def pairwise_leaves(n: int, a: int = 0) -> list[tuple[int, int]]:
@@ -79,6 +79,34 @@ def store_row_order(pos) -> list[int]:
         out.append(pick)
         remaining.remove(pick)
     return out
+
+
+def pairwise_program(n: int) -> list[int]:
+    """Post-order schedule of NumPy's pairwise tree over the leaves of a
+    length-n row: entry i = how many additions follow leaf i (the ancestors
+    whose last leaf is leaf i), each adding the top two pending sums
+    (left + right).  Evaluated with a stack of pending sums."""
+    def walk(n: int, out: list[int]) -> None:
+        if n <= EXACT_ORDER_LEAF:
+            out.append(0)
+            return
+        m = n // 2 - (n // 2) % 8
+        walk(m, out)
+        walk(n - m, out)
+        out[-1] += 1
+    out: list[int] = []
+    walk(n, out)
+    return out
+
+
+def program_depth(prog) -> int:
+    """Largest number of pending sums the schedule holds."""
+    sp = best = 0
+    for adds in prog:
+        sp += 1
+        best = max(best, sp)
+        sp -= adds
+    return best
 
 
 def slot_of(pos: int, n: int) -> int:
@@ -228,10 +256,21 @@ class _Builder:
         cz = -np.longdouble(pre) * mat.astype(np.longdouble).sum(axis=0) - np.longdouble(post)
         rec["cz"] = self.values(cz.astype(np.float64))
         rec["frag"] = rec["col64"] = -1                  # member(): needs the x columns
-        # float32 rows longer than a pairwise leaf: leaf table [n_leaf, qb of
-        # each leaf (10 ints)] in the index table; -1 = one leaf (qb above)
-        rec["leaf"] = (-1 if len(leaves) == 1 else
-                       self.ints(np.concatenate([[len(leaves)], *leaf_qb]).astype(np.int32)))
+        # float32 rows longer than a pairwise leaf: leaf table [n_leaf, then
+        # per leaf its qb (10 ints) and the additions that follow it
+        # (pairwise_program)] in the index table; -1 = one leaf (qb above),
+        # -2 = the tree needs more than EXACT_ORDER_STACK pending sums
+        if len(leaves) == 1:
+            rec["leaf"] = -1
+        else:
+            prog = pairwise_program(n)
+            if program_depth(prog) > EXACT_ORDER_STACK:
+                rec["leaf"] = -2
+            else:
+                table = [len(leaves)]
+                for qb_l, adds in zip(leaf_qb, prog):
+                    table += [int(v) for v in qb_l] + [adds]
+                rec["leaf"] = self.ints(np.asarray(table, dtype=np.int32))
         self.groups.append(rec)
         self.group_src.append((block, cols, scale))
         return len(self.groups) - 1

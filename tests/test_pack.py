@@ -46,20 +46,23 @@ def exact_order_rotate(pk, group, v):
     m4 = (m + 3) // 4 * 4                      # rows 4-padded (float4 loads)
     mat = pk.values_f32[group["mat"]:group["mat"] + m * m4].reshape(m, m4)
     leaf = int(group["leaf"])
+    assert leaf != -2
     if leaf < 0:
-        qbs = [group["qb"]]
-    else:                                      # [n_leaf, qb of each leaf]
+        qbs, prog = [group["qb"]], [0]
+    else:                                      # [n_leaf, (qb[10], additions) per leaf]
         nl = int(pk.index[leaf])
-        qbs = [pk.index[leaf + 1 + 10 * i:leaf + 11 + 10 * i] for i in range(nl)]
+        ents = [pk.index[leaf + 1 + 11 * i:leaf + 12 + 11 * i] for i in range(nl)]
+        qbs, prog = [e[:10] for e in ents], [int(e[10]) for e in ents]
     out = {}
     for r in range(m):
-        s = [_leaf_sum(v, cols, mat, qb, r) for qb in qbs]
-        if len(s) == 1:
-            z = s[0]
-        elif len(s) == 2:
-            z = F32(s[0] + s[1])
-        else:
-            z = F32(s[0] + F32(s[1] + s[2]))
+        stack = []
+        for qb, adds in zip(qbs, prog):        # post-order: leaf, then (left + right)s
+            stack.append(_leaf_sum(v, cols, mat, qb, r))
+            for _ in range(adds):
+                right = stack.pop()
+                stack[-1] = F32(stack[-1] + right)
+        assert len(stack) == 1
+        z = stack[0]
         out[int(rows[r])] = z
     return out
 
@@ -74,7 +77,7 @@ def dense_for(fn, dim, seed):
     return m.rotation.dense() if m.rotation is not None else m.hybrid.chunk_rotations[0]
 
 
-@pytest.mark.parametrize("dim", [2, 5, 8, 9, 10, 13, 30, 50, 100, 128, 129, 200, 250])
+@pytest.mark.parametrize("dim", [2, 5, 8, 9, 10, 13, 30, 50, 100, 128, 129, 200, 250, 300, 520])
 def test_exact_order_schedule_reproduces_numpy(dim):
     disabled = frozenset(range(23, 37)) if dim < 10 else frozenset()
     pk = P.Pack(dim, 1, disabled)
@@ -196,9 +199,12 @@ def test_pairwise_leaves():
     assert P.pairwise_leaves(200) == [(0, 96), (96, 200)]
     assert P.pairwise_leaves(250) == [(0, 120), (120, 184), (184, 250)]
     assert P.pairwise_leaves(256) == [(0, 128), (128, 256)]
-    for n in range(129, 257):                  # the device handles 2 or 3 leaves
-        lv = P.pairwise_leaves(n)
-        assert 2 <= len(lv) <= 3 and lv[0][1] - lv[0][0] <= 128
+    for n in range(129, 969):                  # the device stack holds the whole tree
+        prog = P.pairwise_program(n)
+        assert len(prog) == len(P.pairwise_leaves(n)) and sum(prog) == len(prog) - 1
+        assert P.program_depth(prog) <= P.EXACT_ORDER_STACK
+    assert P.pairwise_program(250) == [0, 0, 2]              # l0 + (l1 + l2)
+    assert P.pairwise_program(512) == [0, 1, 0, 2]           # (l0 + l1) + (l2 + l3)
 
 
 def test_slot_of():

@@ -26,7 +26,7 @@ def assert_close(got, want, prec, what=""):
     assert not bad.any(), (what, prec, np.flatnonzero(bad)[:5], got[bad][:5], want[bad][:5])
 
 
-@pytest.fixture(scope="module", params=[2, 10, 30, 32, 50, 64, 96, 100, 200, 250])
+@pytest.fixture(scope="module", params=[2, 10, 30, 32, 50, 64, 96, 100, 200, 250, 300])
 def pair(request):
     dim = request.param
     eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=4096, seed=0))
