@@ -28,10 +28,6 @@ cudaError_t set_weier_f64(const double* a_then_c);
 cudaError_t set_weier_f32(const float* a_then_c);
 void phase_read_f64(unsigned long long out[8], bool reset);
 void phase_read_f32(unsigned long long out[8], bool reset);
-cudaError_t build_plan_image_f64(const Args<double>& a, int4* out, int n16, size_t smem,
-                                 cudaStream_t stream);
-cudaError_t build_plan_image_f32(const Args<float>& a, int4* out, int n16, size_t smem,
-                                 cudaStream_t stream);
 
 // ------------------------------------------------- on-device population
 // numpy.random.Philox (Philox4x64-10) as numpy runs it: counter starting at
@@ -127,15 +123,7 @@ struct Launch {
   int nbuf = 1;
   int opt_rows = 0;
   size_t smem_nbuf[3] = {0, 0, 0};
-  size_t img_off = 0;      // plan image of this (function, precision) in e->d_plans
-  int img_n16 = 0;
 };
-
-// RB_PLAN_IMAGE=0 makes every CTA build its plan from the pack (load_plan).
-int plan_image_mode() {
-  const char* v = std::getenv("RB_PLAN_IMAGE");
-  return v ? std::atoi(v) : 1;
-}
 
 // RB_PREFETCH=0/1 forces single / double X buffering (default: auto).
 int prefetch_mode() {
@@ -175,7 +163,6 @@ struct rb_engine {
   int32_t* d_index = nullptr;
   double* d_v64 = nullptr;
   float* d_v32 = nullptr;
-  void* d_plans = nullptr;                   // prebuilt plan regions (plan_image_kernel)
   int* h_flags = nullptr;                    // ring of per-call non-finite flags, mapped
   int* d_flags = nullptr;                    // pinned host memory (device alias of h_flags)
   std::atomic<int> next_flag{0};
@@ -201,7 +188,6 @@ void release(rb_engine* e) {
   cudaFree(e->d_index);
   cudaFree(e->d_v64);
   cudaFree(e->d_v32);
-  cudaFree(e->d_plans);
   cudaFree(e->stage_x);
   cudaFree(e->stage_f);
   if (e->pin_x) cudaFreeHost(e->pin_x);
@@ -209,86 +195,6 @@ void release(rb_engine* e) {
   if (e->host_stream) cudaStreamDestroy(e->host_stream);
   cudaSetDevice(prev);
   delete e;
-}
-
-// Kernel arguments that depend on the engine and the (function, precision)
-// only.
-template <class T>
-void base_args(const rb_engine* e, int32_t fn_id, const Launch& L, rb::Args<T>& a) {
-  const int pi = sizeof(T) == 8 ? 0 : 1;
-  a = rb::Args<T>();
-  a.dim = e->dim;
-  a.fns = e->d_fns;
-  a.members = e->d_members;
-  a.segments = e->d_segments;
-  a.groups = e->d_groups;
-  a.index = e->d_index;
-  a.values = reinterpret_cast<const T*>(pi == 0 ? (const void*)e->d_v64 : (const void*)e->d_v32);
-  a.fn = fn_id;
-  a.ldz = e->ldz[pi];
-  a.ldv = L.ldv;
-  a.max_q = L.max_q;
-  a.nbuf = L.nbuf;
-  a.neg_zero = -0.0f;
-  a.opt_rows = L.opt_rows;
-  a.plan_img = e->d_plans ? reinterpret_cast<const int4*>(static_cast<const unsigned char*>(e->d_plans) +
-                                                          L.img_off)
-                          : nullptr;
-  a.plan_n16 = L.img_n16;
-}
-
-// Every enabled (function, precision)'s plan region, built once on the
-// device by load_plan itself (plan_image_kernel) and kept in global memory:
-// a CTA then starts with one coalesced copy instead of a chain of dependent
-// reads (the latency of small batches).
-rb_status build_plan_images(rb_engine* e) {
-  if (!plan_image_mode()) return RB_OK;
-  size_t total = 0;
-  for (size_t fi = 0; fi < e->fns.size(); ++fi) {
-    if (e->fns[fi].category == RB_DISABLED) continue;
-    for (int pi = 0; pi < 2; ++pi) {
-      Launch& L = e->launch[pi][fi];
-      const size_t b = pi == 0 ? rb::plan_bytes<double>(e->dim, L.max_q, L.opt_rows)
-                               : rb::plan_bytes<float>(e->dim, L.max_q, L.opt_rows);
-      L.img_off = total;
-      L.img_n16 = (int)(b / 16);
-      total += b;
-    }
-  }
-  if (total == 0) return RB_OK;
-  void* buf = nullptr;
-  RB_CUDA(cudaMalloc(&buf, total));
-  for (size_t fi = 0; fi < e->fns.size(); ++fi) {
-    if (e->fns[fi].category == RB_DISABLED) continue;
-    for (int pi = 0; pi < 2; ++pi) {
-      const Launch& L = e->launch[pi][fi];
-      int4* out = reinterpret_cast<int4*>(static_cast<unsigned char*>(buf) + L.img_off);
-      const size_t smem = (size_t)L.img_n16 * 16;
-      cudaError_t err;
-      if (pi == 0) {
-        rb::Args<double> a;
-        base_args<double>(e, (int32_t)fi, L, a);
-        a.plan_img = nullptr;
-        err = rb::build_plan_image_f64(a, out, L.img_n16, smem, e->host_stream);
-      } else {
-        rb::Args<float> a;
-        base_args<float>(e, (int32_t)fi, L, a);
-        a.plan_img = nullptr;
-        err = rb::build_plan_image_f32(a, out, L.img_n16, smem, e->host_stream);
-      }
-      if (err != cudaSuccess) {
-        cudaFree(buf);
-        return fail(RB_E_CUDA, std::string("plan image: ") + cudaGetErrorString(err));
-      }
-    }
-  }
-  const cudaError_t err = cudaStreamSynchronize(e->host_stream);
-  if (err != cudaSuccess) {
-    cudaFree(buf);
-    return fail(RB_E_CUDA, std::string("plan image: ") + cudaGetErrorString(err));
-  }
-  e->d_plans = buf;
-  return RB_OK;
 }
 
 // Validation in the reference's order, then the launch on `stream`; the
@@ -321,13 +227,26 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
   int* dflag = e->d_flags + slot;
 
   rb::Args<T> a;
-  base_args<T>(e, fn_id, L, a);
   a.x = x;
   a.f = f;
   a.n = n;
+  a.dim = e->dim;
+  a.fns = e->d_fns;
+  a.members = e->d_members;
+  a.segments = e->d_segments;
+  a.groups = e->d_groups;
+  a.index = e->d_index;
+  a.values = reinterpret_cast<const T*>(pi == 0 ? (const void*)e->d_v64 : (const void*)e->d_v32);
+  a.fn = fn_id;
   a.flag = dflag;
+  a.ldz = e->ldz[pi];
+  a.ldv = L.ldv;
+  a.max_q = L.max_q;
   a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+  a.nbuf = L.nbuf;
   a.l2pf = l2_prefetch();
+  a.neg_zero = -0.0f;
+  a.opt_rows = L.opt_rows;
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
   void* args[] = {&a};
@@ -624,7 +543,6 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
     s = fail(RB_E_CUDA, "mapped flag pointer failed");
   if (s == RB_OK && cudaStreamCreateWithFlags(&e->host_stream, cudaStreamNonBlocking) != cudaSuccess)
     s = fail(RB_E_CUDA, "stream creation failed");
-  if (s == RB_OK) s = build_plan_images(e);
   cudaSetDevice(prev);
   if (s != RB_OK) {
     release(e);

@@ -88,8 +88,6 @@ struct Args {
   int l2pf;         // 1: also pull the tile after the next in-flight one into L2
   int opt_rows;     // member optima staged in shared memory (compositions)
   float neg_zero;   // -0.0f, opaque to ptxas (see f32_leaf)
-  const int4* plan_img;  // prebuilt shared-memory plan of this function (plan_image_kernel), or null
-  int plan_n16;          // its size in 16-byte words
 };
 
 // every writer stores the same value: a plain store (the flag is in mapped
@@ -150,17 +148,6 @@ __host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_
   b += nbuf * align16(sizeof(T) * TP * dim);
   if (sizeof(T) == 4) b += align16(sizeof(T) * TP * ldv);
   b += align16(sizeof(T) * TP * ldz);
-  return b;
-}
-
-// Bytes of the plan region (PlanHead, per-column tables, member optima):
-// everything carve() lays out before the X tile.
-template <class T>
-__host__ __device__ inline size_t plan_bytes(int dim, int max_q, int opt_rows) {
-  size_t b = align16(sizeof(PlanHead));
-  b += 2 * align16(sizeof(int) * max_q) + align16(sizeof(T) * max_q);
-  if (sizeof(T) == 8) b += align16(sizeof(T) * max_q);
-  b += align16(sizeof(T) * opt_rows * dim);
   return b;
 }
 
@@ -988,21 +975,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     evaluate_kernel(const Args<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);
-  if (a.plan_img) {
-    // the plan region, built once per engine by plan_image_kernel: one
-    // coalesced copy instead of load_plan's dependent global reads
-    int4* dst = reinterpret_cast<int4*>(smem_raw);
-    for (int i = threadIdx.x; i < a.plan_n16; i += blockDim.x) dst[i] = __ldg(a.plan_img + i);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s.P->mbar[0])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s.P->mbar[1])));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  } else {
-    load_plan(a, s);
-  }
+  load_plan(a, s);
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;
@@ -1096,18 +1069,6 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     RB_PHASE_ADD(3, c_end - c_tile);
     RB_PHASE_ADD(4, 1);
   }
-}
-
-// Builds the plan region of one function once (rb_initialize): load_plan
-// into shared memory, then the bytes out to global memory for
-// evaluate_kernel to copy.  One CTA of NT threads.
-template <class T>
-__global__ void __launch_bounds__(NT, 1) plan_image_kernel(const Args<T> a, int4* out, int n16) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const Smem<T> s = carve<T>(smem_raw, a);
-  load_plan(a, s);
-  const int4* src = reinterpret_cast<const int4*>(smem_raw);
-  for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
 }
 
 // Host-visible table of instantiations: [0..20] basic kernels, [21] generic.

@@ -19,16 +19,6 @@ extern const void* const kernels_f64[N_VARIANTS] = {
     (const void*)evaluate_kernel<double, 20>, (const void*)evaluate_kernel<double, GENERIC>,
 };
 
-// One function's plan region into global memory (see plan_image_kernel).
-cudaError_t build_plan_image_f64(const Args<double>& a, int4* out, int n16, size_t smem,
-                                   cudaStream_t stream) {
-  cudaError_t err = cudaFuncSetAttribute(plan_image_kernel<double>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  plan_image_kernel<double><<<1, NT, smem, stream>>>(a, out, n16);
-  return cudaGetLastError();
-}
-
 // Series constants of this unit's Weierstrass kernels (rb_kernels.cuh);
 // each translation unit owns its __constant__ copy.
 cudaError_t set_weier_f64(const double* a_then_c) {
