@@ -66,6 +66,9 @@ constexpr int NTC = 2;          // DMMA n-tiles (8 rows) sharing one A fragment 
                                 // (3 measured: +1-3% basic, -10-18% compositions: spills)
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 
+// Kernel arguments: 128 bytes.  Measured: 4-16 more bytes (unused) cost
+// the float64 composition kernels 8-16 % at N = 10^7 (code generation), so
+// anything new must fit inside them.
 template <class T>
 struct Args {
   const T* x;
@@ -89,6 +92,8 @@ struct Args {
   int opt_rows;     // member optima staged in shared memory (compositions)
   float neg_zero;   // -0.0f, opaque to ptxas (see f32_leaf)
 };
+static_assert(sizeof(Args<double>) == 128 && sizeof(Args<float>) == 128,
+              "kernel arguments outgrew 128 bytes (see the note above)");
 
 // every writer stores the same value: a plain store (the flag is in mapped
 // host memory, where device atomics need not be supported)
