@@ -198,3 +198,42 @@ def test_c_abi_rejects_an_empty_batch():
                                 f.ctypes.data_as(ctypes.c_void_p))
     assert st == 7 and f[0] == 7.0
     eng.dispose()
+
+
+def test_concurrent_calls_from_threads():
+    # SURVEY.md 8b threading: the engine is immutable after init and
+    # evaluate may be called concurrently (host arrays and device tensors on
+    # separate streams); results are bit-identical to sequential calls
+    import threading
+    import torch
+    eng = rb.initialize(rb.EngineConfig(dim=30, max_concurrency=2048, seed=6))
+    x = population(30, 1500, seed=6)
+    fns = (0, 9, 24, 31)
+    want = {(fn, p): eng.evaluate(fn, x, precision=p).values for fn in fns for p in ("double", "single")}
+    errors = []
+
+    def worker(k):
+        try:
+            stream = torch.cuda.Stream()
+            xt = torch.from_numpy(x).cuda()
+            torch.cuda.synchronize()              # xt is read on `stream` below
+            for rep in range(6):
+                for fn in fns:
+                    for p in ("double", "single"):
+                        if (rep + k) % 2:
+                            got = eng.evaluate(fn, x, precision=p).values
+                        else:
+                            with torch.cuda.stream(stream):
+                                got = eng.evaluate(fn, xt, precision=p).values.cpu().numpy()
+                        if not np.array_equal(got, want[(fn, p)]):
+                            errors.append((k, rep, fn, p))
+        except Exception as exc:          # pragma: no cover - reported below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    eng.dispose()
+    assert not errors, errors[:5]
