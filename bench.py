@@ -383,15 +383,24 @@ def run_ours(args):
         # resident results buffer through Engine.evaluate(out=...))
         n_chunks = int(os.environ.get("RB_E2E_CHUNKS", "8"))
         n_chunks = n_chunks if world == 1 and shard.count >= n_chunks * 4096 else 1
-        bounds = [shard.count * c // n_chunks for c in range(n_chunks + 1)]
+        # RB_E2E_TAPER=1: small first / last chunks (shorter pipeline fill
+        # -- the first H2D -- and drain -- the last D2H)
+        wts = [1] * n_chunks
+        if os.environ.get("RB_E2E_TAPER", "1") == "1" and n_chunks >= 6:
+            wts = [1, 4] + [8] * (n_chunks - 4) + [4, 1]
+        cum = np.cumsum([0] + wts)
+        bounds = [int(shard.count * int(c) // int(cum[-1])) for c in cum]
         nc_max = max(bounds[c + 1] - bounds[c] for c in range(n_chunks))
         copy_stream = torch.cuda.Stream(device=dev)     # H2D
         out_stream = torch.cuda.Stream(device=dev)      # D2H (PCIe is full duplex)
         res, host_res = {}, {}
         if world == 1:                    # resident results of two chunks in flight
-            res = {p: torch.empty((2, len(fns), nc_max), device=dev,
+            # slot layout [2][len(fns) * nc_max]: chunk c's values for function i
+            # at [i * nc, (i + 1) * nc), so the D2H of a chunk is one contiguous
+            # copy whatever its length
+            res = {p: torch.empty((2, len(fns) * nc_max), device=dev,
                                   dtype=torch.float64 if p == "double" else torch.float32) for p in precs}
-            host_res = {p: torch.empty((2, len(fns), nc_max), dtype=res[p].dtype, pin_memory=True)
+            host_res = {p: torch.empty((2, len(fns) * nc_max), dtype=res[p].dtype, pin_memory=True)
                         for p in precs}
 
         def e2e_step_pipelined():
@@ -415,12 +424,13 @@ def run_ours(args):
                 xcs = {"double": xc, "single": xc.float()}
                 for p in precs:
                     for i, fn in enumerate(fns):
-                        engine.evaluate(fn, xcs[p], p, out=res[p][c % 2, i, :nc])
+                        engine.evaluate(fn, xcs[p], p, out=res[p][c % 2, i * nc:(i + 1) * nc])
                 ev_done[c].record(stream)
                 with torch.cuda.stream(out_stream):
                     out_stream.wait_event(ev_done[c])
                     for p in precs:
-                        host_res[p][c % 2, :, :nc].copy_(res[p][c % 2, :, :nc], non_blocking=True)
+                        host_res[p][c % 2, :len(fns) * nc].copy_(res[p][c % 2, :len(fns) * nc],
+                                                                  non_blocking=True)
                         d2h += len(fns) * nc * res[p].element_size()
                     ev_out[c].record(out_stream)
             stream.wait_stream(copy_stream)
@@ -446,7 +456,7 @@ def run_ours(args):
             ems = float(tt.item())
         e2e = {"value": evals / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
-               "pipeline": (f"{n_chunks} row chunks: H2D of X and D2H of every fitness vector on two "
+               "pipeline": (f"{n_chunks} row chunks (small first and last ones): H2D of X and D2H of every fitness vector on two "
                             "copy streams, overlapped with evaluation" if world == 1 else
                             "H2D, evaluate + NCCL all-gather, D2H per function")}
         del host_x, host_f, host_res, res
