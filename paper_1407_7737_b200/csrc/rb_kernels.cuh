@@ -143,13 +143,15 @@ template <> __device__ __forceinline__ double weier_coord<double>(double zj, con
 template <> __device__ __forceinline__ float weier_coord<float>(float zj, const WeierTab<float>& W) {
   const float w = zj + 0.5f;
   if (!(fabsf(w) * W.c[20] < (float)kTrigBig)) return weier_coord_big<float>(w, W);
+  // sum_k 2^-k cos_k as a Horner chain from k = 20 down (a_k = 0.5^k, so
+  // s * 0.5 is exact): no a_k loads in the loop
   float s = 0.0f;
 #pragma unroll kWeiUnroll
-  for (int k = 0; k < 21; ++k) {
+  for (int k = 20; k >= 0; --k) {
     const float x = W.c[k] * w;
     int q;
     const float r = trig_reduce_pi_f(x, q);
-    s = fmaf(W.a[k], flip_sign(cos_polyf(r * r), q), s);   // a_k = 2^-k: product exact
+    s = fmaf(s, 0.5f, flip_sign(cos_polyf(r * r), q));
   }
   return s;
 }
