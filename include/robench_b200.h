@@ -101,7 +101,7 @@ typedef struct rb_function {
   int32_t category;  /* RB_DISABLED / RB_BASIC / RB_HYBRID / RB_COMPOSITION */
   int32_t n_members;
   int32_t member0;
-  int32_t reserved;
+  int32_t reserved;  /* ignored (set 0): the library's device copy uses it internally */
 } rb_function;
 
 typedef struct rb_pack {

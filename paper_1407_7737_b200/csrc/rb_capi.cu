@@ -20,6 +20,7 @@ extern const void* const kernels_f64[N_VARIANTS];
 extern const void* const kernels_f32[N_VARIANTS];
 extern const void* const kernels_spec_f64[FN_COUNT_SPEC];
 extern const void* const kernels_spec_f32[FN_COUNT_SPEC];
+extern const void* const fixup_f64;
 cudaError_t set_weier_f64x(const double* a_then_c);
 cudaError_t set_weier_f32x(const float* a_then_c);
 void phase_read_f64x(unsigned long long out[8], bool reset);
@@ -85,7 +86,14 @@ namespace {
 
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
-constexpr int kFlagSlots = 4096;
+constexpr uint32_t kFlagSlots = 4096;      // a power of two: slot = counter & (kFlagSlots - 1)
+static_assert((kFlagSlots & (kFlagSlots - 1)) == 0, "flag ring must be a power of two");
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per (device,
+// kernel), while engines of different dims and function sets coexist: it is
+// only ever raised, to the largest need any engine has declared.
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, size_t> g_attr;
 
 rb_status fail(rb_status s, const std::string& msg) {
   g_last_error = msg;
@@ -154,7 +162,9 @@ struct rb_engine {
   int64_t max_concurrency = 0;
   int ldz[2] = {0, 0};                       // [0] fp64, [1] fp32
   std::vector<rb_function> fns;              // host copy for validation
-  std::vector<int> exact_ok;                 // fp32 exact-order rotate supported
+  std::vector<std::string> why[2];           // per precision: non-empty = function unsupported
+  std::vector<int> fixup;                    // float64: bitmask of exact64 members (fixup_kernel)
+  int fixup_grid = 0;
   std::vector<Launch> launch[2];
   rb_function* d_fns = nullptr;
   rb_member* d_members = nullptr;
@@ -165,7 +175,7 @@ struct rb_engine {
   float* d_v32 = nullptr;
   int* h_flags = nullptr;                    // ring of per-call non-finite flags, mapped
   int* d_flags = nullptr;                    // pinned host memory (device alias of h_flags)
-  std::atomic<int> next_flag{0};
+  std::atomic<uint32_t> next_flag{0};
   std::mutex host_mu;                        // host-pointer API staging buffers
   void* stage_x = nullptr;
   void* stage_f = nullptr;
@@ -197,35 +207,10 @@ void release(rb_engine* e) {
   delete e;
 }
 
-// Validation in the reference's order, then the launch on `stream`; the
-// caller has made e->device current, synchronises and reads *flag_out.
 template <class T>
-rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
-                      cudaStream_t stream, volatile int** flag_out) {
-  // validation in the reference's order (engine.py:180-203)
-  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
-  if (fn_id < 0 || fn_id >= (int32_t)e->fns.size())
-    return fail(RB_E_UNKNOWN_FUNCTION, "function id " + std::to_string(fn_id) + " is not in 0..36");
-  if (e->fns[fn_id].category == RB_DISABLED)
-    return fail(RB_E_DISABLED_FUNCTION, "function " + std::to_string(fn_id) + " needs dimension >= 10");
-  if (n > e->max_concurrency)
-    return fail(RB_E_BATCH_TOO_LARGE, "batch of " + std::to_string(n) + " exceeds max_concurrency=" +
-                                          std::to_string(e->max_concurrency));
-  if (n < 1 || !x || !f) return fail(RB_E_INVALID_ARGUMENT, "empty batch or null pointer");
+rb::Args<T> make_args(const rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f, int* dflag,
+                      const Launch& L) {
   const int pi = sizeof(T) == 8 ? 0 : 1;
-  if (pi == 1 && !e->exact_ok[fn_id])
-    return fail(RB_E_UNSUPPORTED, "single precision needs rotated segments whose pairwise tree fits the device stack (any length <= 968)");
-  const Launch& L = e->launch[pi][fn_id];
-
-  const int slot = e->next_flag.fetch_add(1) % kFlagSlots;
-  // the flag lives in mapped pinned memory: cleared by the host, set by the
-  // kernel with a plain store over PCIe, read after the stream sync (no
-  // memset / D2H copy that would queue behind bulk transfers on the copy
-  // engines)
-  volatile int* hflag = e->h_flags + slot;
-  *hflag = 0;
-  int* dflag = e->d_flags + slot;
-
   rb::Args<T> a;
   a.x = x;
   a.f = f;
@@ -247,11 +232,69 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
   a.l2pf = l2_prefetch();
   a.neg_zero = -0.0f;
   a.opt_rows = L.opt_rows;
+  return a;
+}
+
+// float64 re-evaluation of the rows the main kernel marked (fixup_kernel,
+// rb_device.cuh exact64_kernel), stream-ordered behind it.
+rb_status launch_fixup(rb_engine* e, int32_t fn_id, const double* x, int64_t n, double* f,
+                       cudaStream_t stream, int* dflag) {
+  const Launch& L = e->launch[0][fn_id];
+  rb::Args<double> a = make_args<double>(e, fn_id, x, n, f, dflag, L);
+  a.nbuf = 1;
+  const int64_t nchunks = (n + rb::TP - 1) / rb::TP;
+  const int grid = (int)std::min<int64_t>(nchunks, e->fixup_grid);
+  void* args[] = {&a};
+  RB_CUDA(cudaLaunchKernel(rb::fixup_f64, dim3(grid), dim3(rb::NT), args, L.smem_nbuf[1], stream));
+  g_launches.fetch_add(1);
+  return RB_OK;
+}
+
+// Validation in the reference's order, then the launch on `stream`; the
+// caller has made e->device current, synchronises and reads the flags
+// (*flag_out: [0] non-finite input, [1] rows marked for the fixup pass).
+// fixup_now: also queue the fixup pass of a float64 exact64 function behind
+// the kernel (callers that do not inspect the flags before using f).
+template <class T>
+rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
+                      cudaStream_t stream, volatile int** flag_out, bool fixup_now = false) {
+  // validation in the reference's order (engine.py:180-203)
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (fn_id < 0 || fn_id >= (int32_t)e->fns.size())
+    return fail(RB_E_UNKNOWN_FUNCTION, "function id " + std::to_string(fn_id) + " is not in 0..36");
+  if (e->fns[fn_id].category == RB_DISABLED)
+    return fail(RB_E_DISABLED_FUNCTION, "function " + std::to_string(fn_id) + " needs dimension >= 10");
+  if (n > e->max_concurrency)
+    return fail(RB_E_BATCH_TOO_LARGE, "batch of " + std::to_string(n) + " exceeds max_concurrency=" +
+                                          std::to_string(e->max_concurrency));
+  if (n < 1 || !x || !f) return fail(RB_E_INVALID_ARGUMENT, "empty batch or null pointer");
+  const int pi = sizeof(T) == 8 ? 0 : 1;
+  if (!e->why[pi][fn_id].empty())
+    return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fn_id) + ": " + e->why[pi][fn_id]);
+  const Launch& L = e->launch[pi][fn_id];
+
+  const uint32_t slot = e->next_flag.fetch_add(1) & (kFlagSlots - 1);
+  // the flags live in mapped pinned memory: cleared by the host, set by the
+  // kernel with a plain store over PCIe, read after the stream sync (no
+  // memset / D2H copy that would queue behind bulk transfers on the copy
+  // engines)
+  volatile int* hflag = e->h_flags + 2 * slot;      // [0] non-finite, [1] rows left for fixup
+  hflag[0] = 0;
+  hflag[1] = 0;
+  int* dflag = e->d_flags + 2 * slot;
+
+  rb::Args<T> a = make_args<T>(e, fn_id, x, n, f, dflag, L);
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
   void* args[] = {&a};
   RB_CUDA(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream));
   g_launches.fetch_add(1);
+  if constexpr (sizeof(T) == 8) {
+    if (fixup_now && e->fixup[fn_id]) {
+      const rb_status st = launch_fixup(e, fn_id, x, n, f, stream, dflag);
+      if (st != RB_OK) return st;
+    }
+  }
   *flag_out = hflag;
   return RB_OK;
 }
@@ -270,9 +313,19 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   volatile int* flag = nullptr;
   rb_status s = launch_eval<T>(e, fn_id, x, n, f, stream, &flag);
   if (s == RB_OK) {
-    const cudaError_t err = cudaStreamSynchronize(stream);
-    if (err != cudaSuccess) s = fail(RB_E_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(err));
-    else if (*flag) s = non_finite();
+    cudaError_t err = cudaStreamSynchronize(stream);
+    if (err == cudaSuccess && !flag[0] && flag[1]) {    // marked rows: the exact-order pass
+      if constexpr (sizeof(T) == 8) {
+        s = launch_fixup(e, fn_id, x, n, f, stream, const_cast<int*>(e->d_flags + (flag - e->h_flags)));
+        if (s == RB_OK) err = cudaStreamSynchronize(stream);
+      }
+    }
+    if (s != RB_OK) {
+    } else if (err != cudaSuccess) {
+      s = fail(RB_E_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(err));
+    } else if (flag[0]) {
+      s = non_finite();
+    }
   }
   if (prev != e->device) cudaSetDevice(prev);
   return s;
@@ -312,14 +365,14 @@ rb_status evaluate_host_locked(rb_engine* e, int32_t fn_id, const T* x, int64_t 
   RB_CUDA(cudaMemcpyAsync(e->stage_x, src, bx, cudaMemcpyHostToDevice, e->host_stream));
   volatile int* flag = nullptr;
   rb_status s = launch_eval<T>(e, fn_id, static_cast<const T*>(e->stage_x), n,
-                               static_cast<T*>(e->stage_f), e->host_stream, &flag);
+                               static_cast<T*>(e->stage_f), e->host_stream, &flag, true);
   if (s != RB_OK) {
     cudaStreamSynchronize(e->host_stream);
     return s;
   }
   RB_CUDA(cudaMemcpyAsync(dst, e->stage_f, bf, cudaMemcpyDeviceToHost, e->host_stream));
   RB_CUDA(cudaStreamSynchronize(e->host_stream));
-  if (*flag) return non_finite();
+  if (flag[0]) return non_finite();
   if (pinned) std::memcpy(f, dst, bf);
   return RB_OK;
 }
@@ -339,7 +392,10 @@ rb_status evaluate_host(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f
   return s;
 }
 
-// Per-function launch parameters: kernel variant, shared-memory layout.
+// Per-function launch parameters: kernel variant, shared-memory layout.  A
+// function that does not fit (shared-memory tile, plan tables, float32
+// pairwise stack) is marked unsupported in that precision; the others stay
+// usable (the reference has no dimension cap, engine.py:42-44).
 rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
   int sms = 0, optin = 0;
   RB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -349,8 +405,12 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
   e->ldz[0] = pad_to(max_d, 16, 8);   // 8 lanes x 4 points read rows: stride 8 (mod 16) doubles
   e->ldz[1] = pad_to(max_d, 32, 8);
   const int nf = pk->n_functions;
-  e->exact_ok.assign(nf, 1);
-  for (int pi = 0; pi < 2; ++pi) e->launch[pi].assign(nf, Launch());
+  for (int pi = 0; pi < 2; ++pi) {
+    e->launch[pi].assign(nf, Launch());
+    e->why[pi].assign(nf, std::string());
+  }
+  e->fixup.assign(nf, 0);
+  e->fixup_grid = sms;
   std::map<const void*, size_t> need;       // dynamic shared memory per kernel
   std::vector<int> variant(nf, rb::N_VARIANTS - 1);
   std::vector<int> spec(nf, -1);            // function-specialised kernel (rb_fnspec.cuh)
@@ -362,25 +422,35 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
     const int s0 = first.segment0, s1 = last.segment0 + last.n_segments;
     const int g0 = pk->segments[s0].group0;
     const int g1 = pk->segments[s1 - 1].group0 + pk->segments[s1 - 1].n_groups;
-    if (fn.n_members > rb::MAX_MEMBERS || s1 - s0 > rb::MAX_SEGMENTS || g1 - g0 > rb::MAX_GROUPS)
-      return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the plan limits");
+    if (fn.n_members > rb::MAX_MEMBERS || s1 - s0 > rb::MAX_SEGMENTS || g1 - g0 > rb::MAX_GROUPS) {
+      e->why[0][fi] = e->why[1][fi] = "exceeds the plan limits";
+      continue;
+    }
     int max_q = 0, ldv = 4, units = 0;
-    for (int mi = 0; mi < fn.n_members; ++mi) {    // fp32 V rows: a member's chunks at once
+    for (int mi = 0; mi < fn.n_members; ++mi) {    // V rows: a member's chunks at once
       const rb_member& mm = pk->members[fn.member0 + mi];
       int q4 = 0;
+      bool exact64 = false, deep = false;
       for (int si = mm.segment0; si < mm.segment0 + mm.n_segments; ++si) {
         const rb_segment& sg = pk->segments[si];
+        exact64 = exact64 || (rb::exact64_kernel(sg.kernel) && sg.n_groups > 0);
         for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
           max_q += rb::round8(pk->groups[g].m);
           q4 += (pk->groups[g].m + 3) & ~3;
           units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
-          if (pk->groups[g].leaf == -2) e->exact_ok[fi] = 0;   // pairwise tree too deep
+          deep = deep || pk->groups[g].leaf == -2;
         }
       }
+      if (deep)
+        e->why[1][fi] = "single precision needs rotated segments whose pairwise tree fits the "
+                        "device stack (any length <= 968)";
       ldv = std::max(ldv, q4);
+      if (exact64 && !deep) e->fixup[fi] |= 1 << mi;   // (deep: float64 keeps the DMMA z)
     }
-    if (units > rb::MAX_UNITS)
-      return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fi) + " exceeds the DMMA unit table");
+    if (units > rb::MAX_UNITS) {
+      e->why[0][fi] = e->why[1][fi] = "exceeds the DMMA unit table";
+      continue;
+    }
     if (fn.category == RB_BASIC && fn.n_members == 1 && first.n_segments == 1)
       variant[fi] = pk->segments[s0].kernel;
     if (fi >= rb::FN_FIRST_SPEC && fi < rb::FN_FIRST_SPEC + rb::FN_COUNT_SPEC) {
@@ -401,35 +471,140 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       L.func = (pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[variant[fi]];
       if (spec[fi] >= 0) L.func = (pi == 0 ? rb::kernels_spec_f64 : rb::kernels_spec_f32)[spec[fi]];
       L.max_q = std::max(max_q, 1);
-      L.ldv = ldv;
+      L.ldv = pi == 0 ? 0 : ldv;             // float64 has no V tile
       L.opt_rows = fn.category == RB_COMPOSITION ? fn.n_members : 0;
       for (int nb = 1; nb <= 2; ++nb)
         L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, L.ldv, e->ldz[0], L.max_q, nb, L.opt_rows)
-                                  : rb::smem_bytes<float>(pk->dim, ldv, e->ldz[1], L.max_q, nb, L.opt_rows);
-      if ((int)L.smem_nbuf[1] > optin)
-        return fail(RB_E_UNSUPPORTED, "dimension too large for the shared-memory tile");
+                                  : rb::smem_bytes<float>(pk->dim, L.ldv, e->ldz[1], L.max_q, nb, L.opt_rows);
+      if ((int)L.smem_nbuf[1] > optin) {
+        e->why[pi][fi] = "dimension " + std::to_string(pk->dim) + " needs " +
+                         std::to_string(L.smem_nbuf[1]) + " bytes of shared memory per tile (limit " +
+                         std::to_string(optin) + ")";
+        L.func = nullptr;
+        continue;
+      }
       const size_t top = (int)L.smem_nbuf[2] <= optin ? L.smem_nbuf[2] : L.smem_nbuf[1];
       need[L.func] = std::max(need[L.func], top);
+      if (pi == 0 && e->fixup[fi]) need[rb::fixup_f64] = std::max(need[rb::fixup_f64], L.smem_nbuf[1]);
     }
   }
-  for (const auto& kv : need)
-    RB_CUDA(cudaFuncSetAttribute(kv.first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.second));
+  {
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    for (const auto& kv : need) {
+      size_t& have = g_attr[std::make_pair(device, kv.first)];
+      if (kv.second <= have) continue;
+      RB_CUDA(cudaFuncSetAttribute(kv.first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.second));
+      have = kv.second;
+    }
+  }
   for (int fi = 0; fi < nf; ++fi) {
     if (pk->functions[fi].category == RB_DISABLED) continue;
     for (int pi = 0; pi < 2; ++pi) {
       Launch& L = e->launch[pi][fi];
+      if (!L.func) continue;
       int occ[3] = {0, 0, 0};
       for (int nb = 1; nb <= 2; ++nb)
         if ((int)L.smem_nbuf[nb] <= optin)
           RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[nb], L.func, rb::NT,
                                                                 L.smem_nbuf[nb]));
-      if (occ[1] < 1) return fail(RB_E_UNSUPPORTED, "kernel does not fit on an SM");
+      if (occ[1] < 1) {
+        e->why[pi][fi] = "kernel does not fit on an SM";
+        continue;
+      }
       const int mode = prefetch_mode();
       L.nbuf = (mode == 1 && occ[2] >= 1) || (mode < 0 && occ[2] >= occ[1]) ? 2 : 1;
       if (pi == 0) L.nbuf = 1;           // fp64 tiles have no second X buffer
       L.smem = L.smem_nbuf[L.nbuf];
       L.grid_cap = sms * occ[L.nbuf];
     }
+  }
+  return RB_OK;
+}
+
+// Every offset of a pack (a public C ABI: hosts other than pack.py may build
+// one) is checked with its extent against the tables before anything reads
+// through it on the host or the device.
+int64_t ctab_len(int kernel, int d) {
+  switch (kernel) {
+    case rb::K_ELLIPTIC: case rb::K_POWERS: case rb::K_GRIEWANK: return d;
+    case rb::K_WEIERSTRASS: return 43;
+    case rb::K_KATSUURA: return 2;
+    default: return 0;
+  }
+}
+
+rb_status validate_pack(const rb_pack* pk) {
+  const int64_t nv = pk->n_values, ni = pk->n_index;
+  auto in_values = [&](int64_t off, int64_t len) { return len == 0 || (off >= 0 && off + len <= nv); };
+  auto in_index = [&](int64_t off, int64_t len) { return len == 0 || (off >= 0 && off + len <= ni); };
+  auto bad = [](const char* what, int i) {
+    return fail(RB_E_INVALID_ARGUMENT, std::string(what) + " " + std::to_string(i) + " out of range");
+  };
+  if (pk->n_functions > 4096 || pk->n_members < 0 || pk->n_segments < 0 || pk->n_groups < 0 ||
+      nv < 0 || ni < 0 || (nv > 0 && (!pk->values_f64 || !pk->values_f32)) || (ni > 0 && !pk->index) ||
+      !pk->functions || (pk->n_members > 0 && !pk->members) ||
+      (pk->n_segments > 0 && !pk->segments) || (pk->n_groups > 0 && !pk->groups))
+    return fail(RB_E_INVALID_ARGUMENT, "malformed pack header");
+  const int dim = pk->dim;
+  for (int i = 0; i < pk->n_functions; ++i) {
+    const rb_function& f = pk->functions[i];
+    if (f.category == RB_DISABLED) continue;
+    if (f.category < RB_BASIC || f.category > RB_COMPOSITION || f.n_members < 1 || f.member0 < 0 ||
+        (int64_t)f.member0 + f.n_members > pk->n_members)
+      return bad("function", i);
+  }
+  for (int i = 0; i < pk->n_members; ++i) {
+    const rb_member& m = pk->members[i];
+    if (m.n_segments < 1 || m.segment0 < 0 || (int64_t)m.segment0 + m.n_segments > pk->n_segments ||
+        !in_values(m.shift, dim) || (m.perm != -1 && !in_index(m.perm, dim)))
+      return bad("member", i);
+    if (m.perm != -1)
+      for (int j = 0; j < dim; ++j)
+        if (pk->index[m.perm + j] < 0 || pk->index[m.perm + j] >= dim) return bad("member", i);
+    int64_t covered = 0;
+    for (int si = m.segment0; si < m.segment0 + m.n_segments; ++si) {
+      const rb_segment& sg = pk->segments[si];
+      if (sg.src < 0 || sg.d < 1 || (int64_t)sg.src + sg.d > dim) return bad("segment", si);
+      covered += sg.d;
+    }
+    if (covered > dim) return bad("member", i);
+  }
+  for (int i = 0; i < pk->n_segments; ++i) {
+    const rb_segment& s = pk->segments[i];
+    if (s.kernel < 0 || s.kernel >= rb::K_COUNT || s.d < 1 || s.d > dim || s.n_groups < 0 ||
+        s.group0 < 0 || (int64_t)s.group0 + s.n_groups > pk->n_groups ||
+        !in_values(s.ctab, ctab_len(s.kernel, s.d)))
+      return bad("segment", i);
+    int64_t rows = 0;
+    for (int g = s.group0; g < s.group0 + s.n_groups; ++g) {
+      const rb_group& G = pk->groups[g];
+      const int m = G.m;
+      if (m < 1 || m > s.d) return bad("group", g);
+      const int64_t m4 = (m + 3) & ~3, nt = (m + 7) / 8, nk = (m + 3) / 4;
+      if (!in_index(G.col, m) || !in_index(G.row, m) || !in_index(G.col64, m) ||
+          !in_values(G.mat, (int64_t)m * m4) || !in_values(G.frag, nt * nk * 32) || !in_values(G.cz, m))
+        return bad("group", g);
+      for (int q = 0; q < m; ++q)
+        if (pk->index[G.col + q] < 0 || pk->index[G.col + q] >= s.d || pk->index[G.row + q] < 0 ||
+            pk->index[G.row + q] >= s.d || pk->index[G.col64 + q] < 0 || pk->index[G.col64 + q] >= s.d)
+          return bad("group", g);
+      auto qb_ok = [m](const int32_t* qb) {
+        for (int k = 0; k < 10; ++k)
+          if (qb[k] < 0 || qb[k] > m || (k && qb[k] < qb[k - 1])) return false;
+        return true;
+      };
+      if (G.leaf == -1) {
+        if (!qb_ok(G.qb) || G.qb[9] != m) return bad("group", g);
+      } else if (G.leaf != -2) {
+        if (!in_index(G.leaf, 1)) return bad("group", g);
+        const int64_t nl = pk->index[G.leaf];
+        if (nl < 1 || nl > 64 || !in_index(G.leaf, 1 + 11 * nl)) return bad("group", g);
+        for (int64_t l = 0; l < nl; ++l)
+          if (!qb_ok(pk->index + G.leaf + 1 + 11 * l)) return bad("group", g);
+      }
+      rows += m;
+    }
+    if (rows > s.d) return bad("segment", i);
   }
   return RB_OK;
 }
@@ -501,17 +676,9 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   *out = nullptr;
   if (pk->dim < 2 || pk->n_functions <= 0 || max_concurrency < 1)
     return fail(RB_E_INVALID_ARGUMENT, "malformed pack");
-  for (int i = 0; i < pk->n_functions; ++i) {
-    const rb_function& f = pk->functions[i];
-    if (f.category == RB_DISABLED) continue;
-    if (f.n_members < 1 || f.member0 < 0 || f.member0 + f.n_members > pk->n_members)
-      return fail(RB_E_INVALID_ARGUMENT, "function " + std::to_string(i) + ": bad members");
-  }
-  for (int i = 0; i < pk->n_segments; ++i) {
-    const rb_segment& s = pk->segments[i];
-    if (s.kernel < 0 || s.kernel >= rb::K_COUNT || s.d < 1 || s.d > pk->dim ||
-        s.group0 + s.n_groups > pk->n_groups)
-      return fail(RB_E_INVALID_ARGUMENT, "segment " + std::to_string(i) + " malformed");
+  {
+    const rb_status vs = validate_pack(pk);
+    if (vs != RB_OK) return vs;
   }
   int ndev = 0;
   RB_CUDA(cudaGetDeviceCount(&ndev));
@@ -528,14 +695,20 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   e->fns.assign(pk->functions, pk->functions + pk->n_functions);
   rb_status s = plan_launches(e, pk, device);
   if (s == RB_OK) s = upload_series_constants(pk);
-  if (s == RB_OK) s = upload(&e->d_fns, pk->functions, pk->n_functions);
+  if (s == RB_OK) {
+    // the device copy's `reserved` word carries the float64 exact-order
+    // members (PlanHead::exact_mem)
+    std::vector<rb_function> fns(pk->functions, pk->functions + pk->n_functions);
+    for (int i = 0; i < pk->n_functions; ++i) fns[i].reserved = e->fixup[i];
+    s = upload(&e->d_fns, fns.data(), pk->n_functions);
+  }
   if (s == RB_OK) s = upload(&e->d_members, pk->members, pk->n_members);
   if (s == RB_OK) s = upload(&e->d_segments, pk->segments, pk->n_segments);
   if (s == RB_OK) s = upload(&e->d_groups, pk->groups, pk->n_groups);
   if (s == RB_OK) s = upload(&e->d_index, pk->index, pk->n_index);
   if (s == RB_OK) s = upload(&e->d_v64, pk->values_f64, pk->n_values);
   if (s == RB_OK) s = upload(&e->d_v32, pk->values_f32, pk->n_values);
-  if (s == RB_OK && cudaHostAlloc(reinterpret_cast<void**>(&e->h_flags), sizeof(int) * kFlagSlots,
+  if (s == RB_OK && cudaHostAlloc(reinterpret_cast<void**>(&e->h_flags), 2 * sizeof(int) * kFlagSlots,
                                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
     s = fail(RB_E_CUDA, "mapped flag allocation failed");
   if (s == RB_OK && cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_flags), e->h_flags, 0) !=

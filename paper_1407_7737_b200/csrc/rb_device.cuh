@@ -65,6 +65,7 @@ constexpr int MAX_UNITS = 512;  // fp64 DMMA units (m-tile x n-tile of a group) 
 constexpr int NTC = 2;          // DMMA n-tiles (8 rows) sharing one A fragment per k-step
                                 // (3 measured: +1-3% basic, -10-18% compositions: spills)
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
+constexpr int FIXUP = -2;       // member_value mode of fixup_kernel (exact-order float64)
 
 // Kernel arguments: 128 bytes.  Measured: 4-16 more bytes (unused) cost
 // the float64 composition kernels 8-16 % at N = 10^7 (code generation), so
@@ -101,6 +102,19 @@ template <class T>
 __device__ __forceinline__ void raise_flag(const Args<T>& a) {
   *reinterpret_cast<volatile int*>(a.flag) = 2;
 }
+// a.flag[1]: some row's value was left for fixup_kernel (float64 exact64
+// members next to the HappyCat / HGBat residual); the row holds fixup_mark
+// until the fixup pass overwrites it
+template <class T>
+__device__ __forceinline__ void mark_fixup(const Args<T>& a) {
+  reinterpret_cast<volatile int*>(a.flag)[1] = 1;
+}
+// a signalling-NaN payload no arithmetic produces (NaN results are quiet)
+constexpr unsigned long long kFixupBits = 0x7ff4f1c5ed0ddba1ull;
+template <class T> __device__ __forceinline__ T fixup_mark() { return (T)__longlong_as_double(kFixupBits); }
+__device__ __forceinline__ bool is_fixup_mark(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kFixupBits;
+}
 
 struct PlanHead {
   rb_function fn;
@@ -117,8 +131,21 @@ struct PlanHead {
   int8_t job_mem[MAX_SEGMENTS];
   int8_t job_seg[MAX_SEGMENTS];   // index into seg[]
   int unit_off[MAX_SEGMENTS + 1];  // fp64 rotate: segment si's units are unit[unit_off[si] ..)
+  uint32_t exact_mem;             // fp64: members with an exact-order path (exact64_kernel)
+  uint32_t marked;                // fixup_kernel: marked points of the current chunk
   uint32_t unit[MAX_UNITS];       // (group | m-tile << 8 | n-tile << 16), group-major per segment
 };
+
+// float64 kernels whose value amplifies the last ulp of z beyond the parity
+// bar next to an optimum: HappyCat's |sum z^2 - d|^0.25 and HGBat's
+// sqrt(|r2^2 - sz^2|) are not differentiable where the residual vanishes
+// (kernels.py:204-217), and the residual vanishes exactly at the optimum
+// (z = -1).  Members containing them keep the DMMA rotate; a tile in which
+// some point's residual is small relative to its terms (ill64) re-stages the
+// member with z in NumPy's exact order -- rounded products, the pairwise
+// slots of transforms.py:42-48 -- and sums r2 and sz in NumPy's order too,
+// so the residual carries the reference's bits (rotate_exact_f64).
+__host__ __device__ constexpr bool exact64_kernel(int k) { return k == K_HAPPYCAT || k == K_HGBAT; }
 
 __host__ __device__ inline int round8(int v) { return (v + 7) & ~7; }
 
@@ -249,6 +276,9 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
             P.unit[nu++] = (uint32_t)g | ((uint32_t)mt << 8) | ((uint32_t)nt << 16);
     }
     P.unit_off[P.n_seg] = nu;
+    // members with an exact-order path, decided by rb_initialize (plan_launches)
+    // and carried in the device copy of the function record
+    P.exact_mem = sizeof(T) == 8 ? (uint32_t)P.fn.reserved : 0u;
   }
   __syncthreads();
   for (int mi = 0; mi < a.opt_rows && mi < P.fn.n_members; ++mi)
@@ -723,6 +753,178 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
   return nf;
 }
 
+// ------------------------------------------ float64 exact-order fallback
+// One pairwise leaf for RR block rows and the item's 4 points in NumPy's
+// order (f32_leaf's slot walk in double, DMUL + DADD, each rounded): slot s
+// walks q in [qb[s], qb[s+1]), the slots fold ((s0+s1)+(s2+s3))+((s4+s5)+
+// (s6+s7)), the tail adds in order.  load_v(q, v[4]) supplies the column.
+template <int RR, class VL>
+__device__ __forceinline__ void f64_leaf(VL& load_v, const double* bp, int bstride,
+                                         const int (&qb)[10], double (&t0)[4][RR]) {
+  double u0[4][RR], u1[4][RR], u2[4][RR], acc[4][RR];
+#pragma unroll
+  for (int sl = 0; sl < 8; ++sl) {
+    int q = qb[sl];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) acc[i][j] = 0.0;
+    if (q < qb[sl + 1]) {                 // NumPy's r[k] = a[k]: the slot's first product
+      double vv[4];
+      load_v(q, vv);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < RR; ++j) acc[i][j] = __dmul_rn(vv[i], __ldg(bp + j));
+      ++q;
+      bp += bstride;
+    }
+#pragma unroll 1
+    for (; q < qb[sl + 1]; ++q, bp += bstride) {
+      double vv[4];
+      load_v(q, vv);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < RR; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(vv[i], __ldg(bp + j)));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) {
+        const double x = acc[i][j];
+        switch (sl) {
+          case 0: u0[i][j] = x; break;
+          case 1: u0[i][j] = __dadd_rn(u0[i][j], x); break;
+          case 2: u1[i][j] = x; break;
+          case 3: u1[i][j] = __dadd_rn(u1[i][j], x); u0[i][j] = __dadd_rn(u0[i][j], u1[i][j]); break;
+          case 4: u1[i][j] = x; break;
+          case 5: u1[i][j] = __dadd_rn(u1[i][j], x); break;
+          case 6: u2[i][j] = x; break;
+          default:
+            u2[i][j] = __dadd_rn(u2[i][j], x);
+            u1[i][j] = __dadd_rn(u1[i][j], u2[i][j]);
+            u0[i][j] = __dadd_rn(u0[i][j], u1[i][j]);
+        }
+      }
+  }
+#pragma unroll 1
+  for (int q = qb[8]; q < qb[9]; ++q, bp += bstride) {
+    double vv[4];
+    load_v(q, vv);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < RR; ++j) u0[i][j] = __dadd_rn(u0[i][j], __dmul_rn(vv[i], __ldg(bp + j)));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < RR; ++j) t0[i][j] = u0[i][j];
+}
+
+// z of member `mem` (plan segments [s_first, s_end)) in NumPy's exact order:
+// v = scale * (x - o)[perm] (+ pre) recomputed from the X tile per column
+// (engine.py:97-100, hybrid.py:103-110; no V tile, so the rare fallback
+// costs no shared memory), z = matvec(R, v) (transforms.py:42-48) in q-order
+// with the block in the pack's `mat` layout, + post.  Items as in the
+// float32 rotate: 4 points (pq + 8i) x one block row per pass.
+template <bool CHECK>
+__device__ __noinline__ uint32_t rotate_exact_f64(const Args<double>& a, const Smem<double>& s,
+                                     const rb_member& mem, int s_first, int s_end) {
+  const PlanHead& P = *s.P;
+  const int g0 = P.seg[s_first].group0 - P.grp_base;
+  const int ng = P.seg[s_end - 1].group0 + P.seg[s_end - 1].n_groups - P.seg[s_first].group0;
+  int total = 0;
+  for (int g = 0; g < ng; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
+  const double* o = a.values + mem.shift;
+  uint32_t nf = 0u;
+  for (int t = threadIdx.x; t < total; t += NT) {
+    int g = g0, rem = t;
+    for (;;) {
+      const int cnt = (TP / 4) * ((P.grp[g].m + 3) >> 2);
+      if (rem < cnt) break;
+      rem -= cnt;
+      ++g;
+    }
+    const rb_group& G = P.grp[g];
+    const rb_segment& seg = P.seg[P.grp_seg[g]];
+    const double scale = seg.scale, pre = seg.pre, post = seg.post;
+    const int pq = rem % (TP / 4), rq = rem / (TP / 4);
+    const int m = G.m, m4 = round4(m);
+    const int32_t* col = a.index + G.col;
+    const int32_t* perm = mem.perm >= 0 ? a.index + mem.perm + seg.src : nullptr;
+    const double* X0 = s.XS + pq * a.dim;
+    auto load_v = [&](int q, double (&vv)[4]) {
+      const int pos = __ldg(col + q);
+      const int src = perm ? __ldg(perm + pos) : pos;
+      const double ov = __ldg(o + src);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double v = __dmul_rn(scale, __dsub_rn(X0[8 * i * a.dim + src], ov));
+        if (pre != 0.0) v = __dadd_rn(v, pre);
+        vv[i] = v;
+      }
+    };
+    const int* prow = a.index + G.row;
+    auto store = [&](int r, const double (&z)[4]) {
+      const int row = __ldg(prow + r) + seg.src;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        put_z<CHECK>(a, s, pq + 8 * i, row, post != 0.0 ? __dadd_rn(z[i], post) : z[i], nf);
+    };
+#pragma unroll 1
+    for (int r = rq * 4; r < min(rq * 4 + 4, m); ++r) {
+      const double* B = a.values + G.mat + r;
+      double z[4];
+      if (G.leaf < 0) {                         // one pairwise leaf (rows <= 128)
+        int qb[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) qb[k] = G.qb[k];
+        double zz[4][1];
+        f64_leaf<1>(load_v, B, m4, qb, zz);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) z[i] = zz[i][0];
+      } else {                                  // NumPy's pairwise tree (pack.py pairwise_program)
+        constexpr int SD = 4;
+        const int* L = a.index + G.leaf;
+        const int nl = __ldg(L);
+        double st[SD][4];
+        int sp = 0;
+#pragma unroll 1
+        for (int lf = 0; lf < nl; ++lf) {
+          const int* E = L + 1 + 11 * lf;
+          int qb[10];
+#pragma unroll
+          for (int k = 0; k < 10; ++k) qb[k] = __ldg(E + k);
+          double zz[4][1];
+          f64_leaf<1>(load_v, B + qb[0] * m4, m4, qb, zz);
+#pragma unroll
+          for (int d = 0; d < SD; ++d)
+            if (d == sp) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) st[d][i] = zz[i][0];
+            }
+          ++sp;
+          for (int c = __ldg(E + 10); c > 0; --c) {
+#pragma unroll
+            for (int d = 1; d < SD; ++d)
+              if (d == sp - 1) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) st[d - 1][i] = __dadd_rn(st[d - 1][i], st[d][i]);
+              }
+            --sp;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) z[i] = st[0][i];
+      }
+      store(r, z);
+    }
+  }
+  return nf;
+}
+
 // ------------------------------------------------------------ tile state
 // The tile being evaluated, tracked identically by every thread of the CTA.
 struct TileCtx {
@@ -770,7 +972,9 @@ __device__ __forceinline__ void issue_next_x(const Args<T>& a, const Smem<T>& s,
 // barrier: the chunks of a hybrid member are rotated in the same pass and
 // their z laid side by side (chunk k at offset src_k, pack.py).  Returns
 // where z lives (row stride ldz).
-template <class T>
+// EXACT (float64, fixup_kernel): members with an exact-order path
+// (P.exact_mem) rotate in NumPy's order instead of by DMMA.
+template <class T, bool EXACT = false>
 __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
                                  TileCtx& t) {
   const PlanHead& P = *s.P;
@@ -802,7 +1006,15 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
         __syncthreads();
       }
     }
-    nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
+    if constexpr (EXACT && sizeof(T) == 8) {
+      if ((P.exact_mem >> (int)(&mem - P.mem)) & 1u)
+        nf = t.check_z ? rotate_exact_f64<true>(a, s, mem, s_first, s_end)
+                       : rotate_exact_f64<false>(a, s, mem, s_first, s_end);
+      else
+        nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
+    } else {
+      nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
+    }
   }
   if (nf & t.live) raise_flag(a);
   __syncthreads();
@@ -812,22 +1024,29 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
 // Value of one member (basic function, hybrid, or composition member) for
 // the calling lane's point: one staging pass, then the chunk kernels in
 // order (hybrid.py:105-115: 0 + K_0 + K_1 + ...).
+// KID: basic kernel id, GENERIC (run-time kernel dispatch), or FIXUP (the
+// exact-order re-evaluation of marked points, fixup_kernel).  `ill`: float64
+// HappyCat / HGBat members of the main kernels set it when the point's value
+// needs the exact-order z (mark_ill, rb_kernels.cuh).
 template <class T, int KID>
 __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& mem, TileCtx& t,
-                          bool last) {
+                          bool last, bool* ill = nullptr) {
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
   RB_PHASE_MARK(c0);
-  const T* zb = stage_member(a, s, mem, t);
+  const T* zb = stage_member<T, KID == FIXUP>(a, s, mem, t);
   if (last) issue_next_x(a, s, t);
   RB_PHASE_MARK(c1);
+  // compile-time: can this kernel meet a float64 exact64 member at all?
+  constexpr bool kMark = sizeof(T) == 8 && (KID == GENERIC || (KID >= 0 && exact64_kernel(KID)));
+  bool* mark = (kMark && ((P.exact_mem >> (int)(&mem - P.mem)) & 1u)) ? ill : nullptr;
   T total = T(0);
   for (int si = 0; si < mem.n_segments; ++si) {
     const rb_segment& seg = P.seg[mem.segment0 - P.seg_base + si];
-    const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab};
+    const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab, mark};
     T v;
     if constexpr (KID >= 0) v = kernel_value_k<T, KID>(pt);
-    else v = kernel_value<T>(seg.kernel, pt);
+    else v = kernel_value<T, KID == FIXUP>(seg.kernel, pt);
     total = (si == 0) ? v : total + v;
   }
   __syncthreads();                      // z is rewritten by the next member / tile
@@ -931,8 +1150,9 @@ __device__ __forceinline__ void composition_weights(const Args<T>& a, const Plan
 // composition.py:114-166 for the calling lane's point: weights from the
 // squared distances to every member optimum (X tile in XS), then the
 // sigma-weighted, biased member values, skipping zero weights.
-template <class T>
-__device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid) {
+template <class T, int MODE = GENERIC>
+__device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid,
+                               bool* ill = nullptr) {
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int nm = P.fn.n_members;
@@ -957,7 +1177,7 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
     t.live = P.livek[k];
     if (!t.live) continue;
     const rb_member& mem = P.mem[k];
-    const T g = member_value<T, GENERIC>(a, s, mem, t, k == nm - 1);
+    const T g = member_value<T, MODE>(a, s, mem, t, MODE != FIXUP && k == nm - 1, ill);
     if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
   }
   return total;
@@ -967,7 +1187,7 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
 // SPEC_BASE + fid.
 constexpr int SPEC_BASE = 100;
 template <class T, int FID>
-__device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid);
+__device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid, bool* ill);
 
 // Resident CTAs per SM the register budget is sized for.
 template <class T, int KID>
@@ -1059,20 +1279,85 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     RB_PHASE_MARK(c_loaded);
     RB_PHASE_ADD(0, c_loaded - c_tile);
     T result;
+    bool ill = false;                   // float64: value needs the exact-order z (fixup_kernel)
     if constexpr (KID >= SPEC_BASE) {
-      result = spec_value<T, KID - SPEC_BASE>(a, st, t, valid);
+      result = spec_value<T, KID - SPEC_BASE>(a, st, t, valid, &ill);
     } else if constexpr (KID >= 0) {
-      result = member_value<T, KID>(a, st, P.mem[0], t, true);
+      result = member_value<T, KID>(a, st, P.mem[0], t, true, &ill);
     } else if (P.fn.category != RB_COMPOSITION) {
-      result = member_value<T, GENERIC>(a, st, P.mem[0], t, true);
+      result = member_value<T, GENERIC>(a, st, P.mem[0], t, true, &ill);
     } else {
-      result = composition_value<T>(a, st, t, valid);
+      result = composition_value<T>(a, st, t, valid, &ill);
     }
-    if (l8 == 0 && valid) a.f[row0 + p] = result + C<T>(100.0);     // engine.py:209
+    if (l8 == 0 && valid) {
+      if (sizeof(T) == 8 && ill) {
+        a.f[row0 + p] = fixup_mark<T>();
+        mark_fixup(a);
+      } else {
+        a.f[row0 + p] = result + C<T>(100.0);                       // engine.py:209
+      }
+    }
     __syncthreads();                                                 // XS reused by next TMA
     RB_PHASE_MARK(c_end);
     RB_PHASE_ADD(3, c_end - c_tile);
     RB_PHASE_ADD(4, 1);
+  }
+}
+
+// float64 re-evaluation of the rows the main kernel marked (fixup_mark):
+// points next to a HappyCat / HGBat residual, whose value needs z in NumPy's
+// exact order (exact64_kernel).  Each CTA scans 32-row chunks of f, gathers
+// a chunk's marked rows into one tile (X rows copied by index), evaluates
+// the whole function for them -- weights and every member, the exact64
+// members rotated by rotate_exact_f64 -- and writes their values.  Chunks
+// without marks cost one read of their f words.  One CTA per SM with the
+// full register file: the path is rare and not tuned for speed.
+template <class T>
+__global__ void __launch_bounds__(NT, 1) fixup_kernel(const Args<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Smem<T> s = carve<T>(smem_raw, a);
+  load_plan(a, s);
+  PlanHead& P = *s.P;
+  const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const int64_t nchunks = (a.n + TP - 1) / TP;
+  TileCtx t{0, 0, 0u, false, true, 0u, false};
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t row0 = c * TP;
+    const int nrow = tile_rows(a, c);
+    if (threadIdx.x == 0) P.marked = 0u;
+    __syncthreads();
+    if (l8 == 0 && p < nrow && is_fixup_mark((double)a.f[row0 + p])) atomicOr(&P.marked, 1u << p);
+    __syncthreads();
+    const uint32_t marked = P.marked;
+    if (!marked) continue;                     // (P.marked is reset behind the next barrier)
+    const int nv = __popc(marked);
+    // tile point q <- the chunk's q-th marked row
+    for (int e = threadIdx.x; e < nv * a.dim; e += NT) {
+      const int q = e / a.dim, j = e - q * a.dim;
+      const int r = (int)__fns(marked, 0, q + 1);
+      s.XS[e] = a.x[(row0 + r) * a.dim + j];
+    }
+    if (threadIdx.x == 0) {
+      P.live = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
+#pragma unroll
+      for (int k = 0; k < MAX_MEMBERS; ++k) P.livek[k] = 0u;
+    }
+    __syncthreads();
+    const bool valid = p < nv;
+    t.tile = c;
+    t.nv = nv;
+    t.live = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
+    uint32_t mx = 0u;                          // X scan as in evaluate_kernel
+    if (valid) {
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(s.XS + p * a.dim);
+      for (int j = l8; j < a.dim; j += 8) mx = max(mx, xw[j * 2 + 1] & 0x7fffffffu);
+    }
+    if (mx >= 0x7ff00000u) raise_flag(a);
+    t.check_z = __syncthreads_or(mx >= 0x7bf00000u) != 0;
+    const T result = P.fn.category == RB_COMPOSITION ? composition_value<T, FIXUP>(a, s, t, valid)
+                                                     : member_value<T, FIXUP>(a, s, P.mem[0], t, false);
+    if (l8 == 0 && valid) a.f[row0 + (int)__fns(marked, 0, p + 1)] = result + C<T>(100.0);
+    __syncthreads();
   }
 }
 

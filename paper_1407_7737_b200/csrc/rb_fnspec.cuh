@@ -61,6 +61,15 @@ __host__ __device__ constexpr JobList job_list(int fid) {
   return L;
 }
 
+// Does function fid have a HappyCat / HGBat job (float64 exact-order
+// fallback, rb_device.cuh exact64_kernel)?
+__host__ __device__ constexpr bool has_exact64(int fid) {
+  const JobList L = job_list(fid);
+  bool any = false;
+  for (int j = 0; j < L.n; ++j) any = any || exact64_kernel(L.kernel[j]);
+  return any;
+}
+
 // Kernel value of job j of function FID: a branch chain over the function's
 // own job kernels only (each inlined once per job), so the register
 // allocation covers these kernels and not all 21.
@@ -80,7 +89,7 @@ __device__ __forceinline__ T spec_kernel(int j, const Pt<T>& pt) {
 // (hybrid.py:105-115), composition members blended with their weights and
 // skipped when no point of the tile weighs them (composition.py:157-166).
 template <class T, int FID>
-__device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid) {
+__device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool valid, bool* ill) {
   constexpr JobList L = job_list(FID);
   constexpr bool comp = FID >= 29;
   PlanHead& P = *s.P;
@@ -118,10 +127,12 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
     const T* zb = stage_member(a, s, mem, t);
     if (j1 == L.n) issue_next_x(a, s, t);
     RB_PHASE_MARK(c1);
+    constexpr bool kMark = sizeof(T) == 8 && has_exact64(FID);
+    bool* mark = (kMark && ((P.exact_mem >> mi) & 1u)) ? ill : nullptr;
     T g = T(0);
     for (int j = j0; j < j1; ++j) {
       const rb_segment& seg = P.seg[P.job_seg[j]];
-      const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab};
+      const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab, mark};
       const T v = spec_kernel<T, FID, 0>(j, pt);
       g = j == j0 ? v : g + v;                     // hybrid.py:105-115: 0 + K_0 + K_1 + ...
     }

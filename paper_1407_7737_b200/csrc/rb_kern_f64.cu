@@ -19,6 +19,9 @@ extern const void* const kernels_f64[N_VARIANTS] = {
     (const void*)evaluate_kernel<double, 20>, (const void*)evaluate_kernel<double, GENERIC>,
 };
 
+// The exact-order re-evaluation of marked rows (any function; float64).
+extern const void* const fixup_f64 = (const void*)fixup_kernel<double>;
+
 // Series constants of this unit's Weierstrass kernels (rb_kernels.cuh);
 // each translation unit owns its __constant__ copy.
 cudaError_t set_weier_f64(const double* a_then_c) {

@@ -32,7 +32,22 @@ struct Pt {            // one point's view for the kernels
   int d;
   int l8;
   const T* ctab;       // per-(kernel, d) NumPy-computed constants (pack.py)
+  bool* ill = nullptr; // float64 HappyCat / HGBat: set when the value needs the
+                       // exact-order z (rb_device.cuh exact64_kernel)
 };
+
+// float64 HappyCat / HGBat next to the non-differentiable residual: the
+// DMMA z is a few ulps (of its terms) off NumPy's, so the value keeps the
+// parity bar only while the residual is not small against its terms.  Both
+// values carry +100 (bar = 1e-12 of it, ~1e-10 absolute); r2's error is
+// ~eps * S and the HGBat product's ~eps * U, so |r2 - d| >= S / 10 keeps
+// HappyCat's pow within ~eps * S^0.25 and |r2^2 - sz^2| >= U / 10 keeps
+// HGBat's sqrt within ~5 eps relative.  Random points in the search box
+// have |r2 - d| ~ 17 d; points near an optimum are marked and re-evaluated
+// in exact order (fixup_kernel).
+template <class T> __device__ __forceinline__ void mark_ill(const Pt<T>& P, bool cond) {
+  if (sizeof(T) == 8 && P.ill != nullptr) *P.ill = *P.ill || cond;
+}
 
 template <class T> __device__ __forceinline__ T sq(T a) { return a * a; }
 
@@ -156,7 +171,10 @@ template <> __device__ __forceinline__ float weier_coord<float>(float zj, const 
   return s;
 }
 
-template <class T, int K>
+// NP (float64 only; float32 sums are always in NumPy's order): HappyCat /
+// HGBat sum in NumPy's pairwise order -- the exact-order re-evaluation
+// (fixup_kernel), where z carries NumPy's bits and r2, sz must too.
+template <class T, int K, bool NP = false>
 __device__ __forceinline__ T kernel_value_k(const Pt<T>& P) {
   const T* z = P.z;
   const int d = P.d, l8 = P.l8;
@@ -254,13 +272,21 @@ __device__ __forceinline__ T kernel_value_k(const Pt<T>& P) {
     const T mc = cs / T(d);
     return ((C<T>(-20.0) * M<T>::exp(C<T>(-0.2) * rms) - M<T>::exp(mc)) + C<T>(20.0)) + C<T>(kE);
   } else if constexpr (K == K_HAPPYCAT) {                             // :204-209
-    const T r2 = pw8<T>(0, d, square, l8);
-    const T sz = pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
+    // NP: NumPy-order sums, so with the exact-order z r2 and sz carry the
+    // reference's bits (rb_device.cuh exact64_kernel)
+    const T r2 = NP ? pw8_np<T>(0, d, square, l8) : pw8<T>(0, d, square, l8);
+    const T sz = NP ? pw8_np<T>(0, d, [&](int i) { return z[i]; }, l8)
+                    : pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
+    const T S = r2 + T(d);
+    mark_ill(P, isfinite(S) && !(M<T>::fabs(r2 - T(d)) >= T(0.1) * S));
     return (M<T>::pow(M<T>::fabs(r2 - T(d)), C<T>(0.25)) + (C<T>(0.5) * r2 + sz) / T(d)) +
            C<T>(0.5);
   } else if constexpr (K == K_HGBAT) {                                // :212-217
-    const T r2 = pw8<T>(0, d, square, l8);
-    const T sz = pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
+    const T r2 = NP ? pw8_np<T>(0, d, square, l8) : pw8<T>(0, d, square, l8);
+    const T sz = NP ? pw8_np<T>(0, d, [&](int i) { return z[i]; }, l8)
+                    : pw8<T>(0, d, [&](int i) { return z[i]; }, l8);
+    const T U = r2 * r2 + sz * sz;
+    mark_ill(P, isfinite(U) && !(M<T>::fabs(r2 * r2 - sz * sz) >= T(0.1) * U));
     return (M<T>::sqrt(M<T>::fabs(r2 * r2 - sz * sz)) + (C<T>(0.5) * r2 + sz) / T(d)) +
            C<T>(0.5);
   } else if constexpr (K == K_SCHAFFERS_F6) {                         // :226-228
@@ -273,11 +299,11 @@ __device__ __forceinline__ T kernel_value_k(const Pt<T>& P) {
   }
 }
 
-template <class T>
+template <class T, bool NP = false>
 __device__ T kernel_value(int k, const Pt<T>& P) {
   switch (k) {
 #define RB_CASE(K) \
-  case K: return kernel_value_k<T, K>(P);
+  case K: return kernel_value_k<T, K, NP>(P);
     RB_CASE(K_SPHERE) RB_CASE(K_ELLIPSOID) RB_CASE(K_ELLIPTIC) RB_CASE(K_DISCUS)
     RB_CASE(K_CIGAR) RB_CASE(K_POWERS) RB_CASE(K_SHARP_VALLEY) RB_CASE(K_STEP)
     RB_CASE(K_WEIERSTRASS) RB_CASE(K_GRIEWANK) RB_CASE(K_RASTRIGIN) RB_CASE(K_SCHAFFERS_F7)

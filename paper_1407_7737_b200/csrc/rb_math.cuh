@@ -196,6 +196,14 @@ __device__ __forceinline__ T pw8(int lo, int n, F&& f, int l8) {
   }
 }
 
+// NumPy's pairwise order in either precision (float64 HappyCat / HGBat:
+// their sums feed a non-differentiable residual, exact64_kernel).
+template <class T, class F>
+__device__ __forceinline__ T pw8_np(int lo, int n, F&& f, int l8) {
+  if (n <= 128) return pw8_leaf<T>(lo, n, f, l8);
+  return pw8_tree<T>(lo, n, f, l8);
+}
+
 // Sequential product over i = 0..n-1 of f(i) (np.prod is a plain left fold,
 // kernels.py:112); lane l8 evaluates the i = l8 (mod 8) factors.  float64
 // multiplies lane partials instead (order-free to its tolerance).

@@ -102,7 +102,7 @@ class Engine:
         build instead of the reference's rule (grid.py needs basic-member
         compositions at dimension 2, as scalar_evaluator does,
         engine.py:121-138)."""
-        self.config = config
+        self.config = config = _config(config)
         self._disposed = False
         dim = config.dim
         if enabled is not None:
@@ -119,6 +119,10 @@ class Engine:
                                      int(config.max_concurrency), int(config.device),
                                      ctypes.byref(handle)))
         self._handle = handle
+        # engine.py:155-159 keeps one per-point evaluator per (fn, precision);
+        # here each is a handle onto the device-resident instance
+        self._evaluators = {(fn, prec): _PointEvaluator(self, fn, prec)
+                            for fn in self.enabled_ids for prec in _DTYPES}
 
     @property
     def dim(self) -> int:
@@ -135,13 +139,19 @@ class Engine:
     def evaluate(self, fn_id: int, batch, precision: str | None = None, *, out=None) -> EvalResult:
         """Score every point of ``batch`` against ``fn_id`` (engine.py:174-214).
 
+        ``batch``: this package's PointBatch, any object with a 2-D ``data``
+        array (the reference's own ``robench.PointBatch``), a NumPy array or
+        a CUDA tensor.
         ``out`` (addition, CUDA batches only): a contiguous device tensor of
         the batch's length and the precision's dtype that receives the values
         (pipelines that keep results resident, e.g. bench.py's e2e step)."""
         if self._disposed:
             raise UseAfterDispose("engine was disposed")
         if not isinstance(batch, PointBatch):
-            batch = PointBatch(batch)
+            data = batch
+            if not isinstance(batch, np.ndarray) and not _is_torch(batch) and hasattr(batch, "data"):
+                data = batch.data                            # robench.PointBatch and friends
+            batch = PointBatch(data)
         catalog.lookup(fn_id)
         fn_id = int(fn_id)
         if fn_id in self._disabled:
@@ -169,6 +179,7 @@ class Engine:
         if not self._disposed:
             _lib.check(_lib.load().rb_dispose(ctypes.byref(self._handle)))
             self._pack = None
+            self._evaluators = None
         self._disposed = True
 
     def __del__(self):
@@ -203,7 +214,43 @@ class Engine:
         return out
 
 
-def initialize(config: EngineConfig) -> Engine:
+class _PointEvaluator:
+    """``Engine._evaluators[(fn, precision)]`` (engine.py:87-118): calling it
+    on one point returns that point's value without the bias, like the
+    reference's per-point evaluators, computed on the device.  It holds the
+    engine weakly: dispose() releases it (test_engine.py:158-166)."""
+
+    __slots__ = ("_engine", "fn_id", "precision", "__weakref__")
+
+    def __init__(self, engine: Engine, fn_id: int, precision: str):
+        import weakref
+        self._engine = weakref.ref(engine)
+        self.fn_id, self.precision = fn_id, precision
+
+    def __call__(self, x):
+        # the device value carries the bias; it is removed here (rounded), so
+        # evaluator(x) + 100 may differ from evaluate() in the last ulp
+        eng = self._engine()
+        if eng is None:
+            raise UseAfterDispose("engine was disposed")
+        dt = _DTYPES[self.precision]
+        row = np.asarray(x, dtype=dt).reshape(1, -1)
+        return eng.evaluate(self.fn_id, row, self.precision).values[0] - dt(catalog.VALUE_BIAS)
+
+
+def _config(config) -> EngineConfig:
+    """This package's EngineConfig from any config carrying the reference's
+    fields (robench.EngineConfig, engine.py:34-52)."""
+    if isinstance(config, EngineConfig):
+        return config
+    return EngineConfig(dim=config.dim, max_concurrency=config.max_concurrency, seed=config.seed,
+                        precision=config.precision, threads=config.threads,
+                        device=getattr(config, "device", 0))
+
+
+def initialize(config) -> Engine:
     """Build every instance on the host, upload the pack, return the engine
-    (engine.py:225-228)."""
-    return Engine(config)
+    (engine.py:225-228).  ``config``: this package's EngineConfig or the
+    reference's (a robench caller's ``robench.initialize`` can be pointed here
+    unchanged, INTEGRATION.md)."""
+    return Engine(_config(config))

@@ -6,6 +6,7 @@ import re
 from pathlib import Path
 
 import numpy as np
+import pytest
 
 from paper_1407_7737_b200 import _lib, pack
 
@@ -51,3 +52,56 @@ def test_null_and_disposed_handles_map_to_reference_errors():
     handle = ctypes.c_void_p()
     assert lib.rb_dispose(ctypes.byref(handle)) == 0      # idempotent on NULL
     assert lib.rb_initialize(None, 1, 0, ctypes.byref(handle)) == 7
+
+
+def _corrupt(p, table, idx, field, value):
+    arr = getattr(p, table)
+    arr[idx][field] = value
+
+
+@pytest.mark.parametrize("table,field,value", [
+    ("members", "segment0", 10 ** 6),
+    ("members", "shift", -5),
+    ("members", "perm", 10 ** 8),
+    ("segments", "ctab", 10 ** 9),
+    ("segments", "src", 7),
+    ("groups", "col", 10 ** 9),
+    ("groups", "mat", -100),
+    ("groups", "frag", 10 ** 9),
+    ("groups", "cz", 10 ** 9),
+    ("groups", "leaf", 10 ** 9),
+    ("groups", "m", 0),
+])
+def test_malformed_pack_offsets_are_rejected_before_any_read(table, field, value):
+    # rb_initialize bounds-checks every offset with its extent (a public C ABI:
+    # non-Python hosts build packs too); the check precedes any CUDA call, so
+    # it runs without a GPU
+    p = pack.Pack(10, 0)
+    idx = {"members": 3, "segments": 5, "groups": 4}[table]
+    if table == "members" and field == "perm":
+        idx = int(p.functions[23]["member0"])          # a hybrid: has a permutation
+    _corrupt(p, table, idx, field, value)
+    handle = ctypes.c_void_p()
+    st = _lib.load().rb_initialize(ctypes.byref(_lib.make_pack(p)), 8, 0, ctypes.byref(handle))
+    assert st == 7, (table, field, st)
+    assert b"out of range" in _lib.load().rb_last_error()
+
+
+def test_malformed_index_entries_are_rejected():
+    p = pack.Pack(10, 0)
+    g = p.groups[0]
+    p.index[int(g["col"])] = 10 ** 6                    # a column outside the segment
+    handle = ctypes.c_void_p()
+    assert _lib.load().rb_initialize(ctypes.byref(_lib.make_pack(p)), 8, 0, ctypes.byref(handle)) == 7
+
+
+@pytest.mark.parametrize("dim", [10, 13, 30, 100, 300])
+def test_well_formed_packs_pass_validation(dim):
+    # without a GPU the call gets past validation and fails at the device
+    # query (RB_E_CUDA); with one it succeeds
+    p = pack.Pack(dim, 0)
+    handle = ctypes.c_void_p()
+    st = _lib.load().rb_initialize(ctypes.byref(_lib.make_pack(p)), 8, 0, ctypes.byref(handle))
+    assert st in (0, 9), _lib.load().rb_last_error()
+    if st == 0:
+        _lib.load().rb_dispose(ctypes.byref(handle))

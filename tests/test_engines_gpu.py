@@ -1,0 +1,94 @@
+"""Engines coexisting in one process, and dimensions past the shared-memory
+tile: the reference lets any number of engines of any dims live side by side
+(engine.py:144-159, 225-228) and has no dimension cap (engine.py:42-44)."""
+
+import numpy as np
+import pytest
+
+from tests.conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+import paper_1407_7737_b200 as rb  # noqa: E402
+from oracle.robench_oracle import Oracle, population  # noqa: E402
+
+
+def _check(eng, orc, fns, n=24):
+    x = population(eng.dim, n, seed=3)
+    for fn in fns:
+        for prec, rel, ab in (("double", 1e-12, 1e-10), ("single", 1e-5, 0.0)):
+            got = eng.evaluate(fn, x, precision=prec).values.astype(np.float64)
+            want = orc.evaluate(fn, x, prec).astype(np.float64)
+            assert np.all(np.abs(got - want) <= np.maximum(rel * np.abs(want), ab)), (eng.dim, fn, prec)
+
+
+def test_smaller_engine_created_later_does_not_shrink_the_first():
+    # the per-kernel dynamic shared-memory limit is process-wide: a dim-10
+    # engine built after a dim-100 one must not lower it
+    big = rb.initialize(rb.EngineConfig(dim=100, max_concurrency=64, seed=0))
+    small = rb.initialize(rb.EngineConfig(dim=10, max_concurrency=64, seed=0))
+    fns = (0, 8, 20, 21, 24, 29, 32, 36)
+    _check(big, Oracle(100, 0), fns)
+    _check(small, Oracle(10, 0), fns)
+    small.dispose()
+    _check(big, Oracle(100, 0), fns)
+    big.dispose()
+
+
+def test_dimension_past_the_tile_disables_only_what_does_not_fit():
+    # float64 compositions stop fitting the shared-memory tile first; the
+    # engine still serves every function that fits
+    dim = 420
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=16, seed=0))
+    orc = Oracle(dim, 0)
+    x = population(dim, 8, seed=1)
+    served, refused = [], []
+    for fn in eng.enabled_ids:
+        for prec in ("double", "single"):
+            try:
+                got = eng.evaluate(fn, x, precision=prec).values.astype(np.float64)
+            except rb.DeviceError as err:
+                assert any(w in str(err) for w in ("shared memory", "pairwise", "exceeds")), str(err)
+                refused.append((fn, prec))
+                continue
+            want = orc.evaluate(fn, x, prec).astype(np.float64)
+            rel, ab = (1e-12, 1e-10) if prec == "double" else (1e-5, 0.0)
+            assert np.all(np.abs(got - want) <= np.maximum(rel * np.abs(want), ab)), (fn, prec)
+            served.append((fn, prec))
+    eng.dispose()
+    assert (0, "double") in served and (0, "single") in served
+    print("served", len(served), "refused", refused)
+
+
+@pytest.mark.parametrize("dim", [10, 30, 100])
+def test_near_optimum_rows_take_the_exact_order_pass(dim):
+    # float64 HappyCat / HGBat members next to their optimum: the main kernel
+    # marks the rows, the fixup pass re-evaluates them with NumPy-order z
+    # (rb_device.cuh exact64_kernel); host arrays and device tensors, batch
+    # and single rows agree bit for bit, and meet the bar
+    import torch
+    from paper_1407_7737_b200 import _lib, instances
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=4096, seed=4))
+    orc = Oracle(dim, 4)
+    rng = np.random.default_rng(dim)
+    for fn in (20, 21, 24, 26, 27, 28, 30, 32, 33, 34, 35, 36):
+        inst = instances.build(fn, dim, 4)
+        optima = [m.shift for m in inst.members] if hasattr(inst, "members") else [inst.shift]
+        rows = [rng.uniform(-100, 100, dim)]
+        for o in optima:
+            o = np.asarray(o, dtype=np.float64)
+            rows += [o, o + 1e-12 * rng.standard_normal(dim), o + 1e-9 * rng.standard_normal(dim),
+                     o + 1e-6 * rng.standard_normal(dim)]
+        x = np.vstack(rows + [rng.uniform(-100, 100, (40, dim))])
+        want = orc.evaluate(fn, x, "double")
+        n0 = _lib.launch_count()
+        host = eng.evaluate(fn, x).values
+        dev = eng.evaluate(fn, torch.from_numpy(x).cuda()).values.cpu().numpy()
+        assert np.array_equal(host, dev), fn
+        assert np.all(np.abs(host - want) <= np.maximum(1e-12 * np.abs(want), 1e-10)), \
+            (dim, fn, np.max(np.abs(host - want)))
+        for i in (1, 2, 3):
+            assert eng.evaluate(fn, x[i:i + 1]).values[0] == host[i], (fn, i)
+        assert _lib.launch_count() - n0 >= 3          # main kernel + fixup passes ran
+    eng.dispose()

@@ -6,15 +6,17 @@ inf / nan there, no error: kernels.py:45-49 checks z only).  Oracle =
 the CPU restatement; tolerances as in test_parity_gpu.py, with equal
 infinities / NaNs counting as equal.
 
-float32 z is bit-exact (NumPy's summation order), so float32 holds the
-1e-5 bar on every row.  float64 z is the DMMA sum, within an ulp or so of
-NumPy's but not bit-identical; two row classes are
-ill-conditioned for that: 1e-9 off an optimum, HappyCat / HGBat's
-|sum z^2 - d|^0.25 has a derivative ~1e7 (measured deviation 7e-10
-absolute), and at |x| ~ 1e6 (10^4 x outside the search box) Weierstrass
-multiplies a z difference by 2 pi 1.5^20 ~ 2e4 (measured 6e-10 relative).
-Those float64 rows are held to 1e-8 relative; every other row to the
-north-star bar."""
+Every row inside or near the search box -- random, origin, exact optima,
+1e-9 and 1e-3 off an optimum, |x| ~ 1e3 -- is held to the north-star bar in
+both precisions.  float32 z is bit-exact (NumPy's summation order); float64
+z is the DMMA sum (within an ulp of NumPy's) except for HappyCat / HGBat
+members, whose |sum z^2 - d|^0.25 / sqrt(|r2^2 - sz^2|) would turn that ulp
+into ~1e-9 next to an optimum: those members rotate and sum in NumPy's exact
+order in float64 as well (rb_device.cuh exact64_kernel).
+
+Rows at |x| ~ 1e6 (10^4 x outside the search box, where Weierstrass
+multiplies a z difference by 2 pi 1.5^20 ~ 2e4) are reported separately:
+float64 holds them to 1e-8 relative and the measured worst case is printed."""
 
 import numpy as np
 import pytest
@@ -49,16 +51,27 @@ def _optima(fn, dim, seed):
 
 
 def _special_points(fn, dim, seed):
-    """(points, ill-conditioned-for-float64 mask)"""
+    """(points, far-outside-the-box mask)"""
     rng = np.random.default_rng(1000 + fn)
-    pts, ill = [np.zeros(dim)], [False]
+    pts, far = [np.zeros(dim)], [False]
     for o in _optima(fn, dim, seed):
         o = np.asarray(o, dtype=np.float64)
         pts += [o, o + 1e-9 * rng.standard_normal(dim), o + 1e-3 * rng.standard_normal(dim)]
-        ill += [False, True, False]
+        far += [False, False, False]
     pts += [rng.uniform(-1e3, 1e3, dim), rng.uniform(-1e6, 1e6, dim)]
-    ill += [False, True]
-    return np.vstack(pts), np.array(ill)
+    far += [False, True]
+    return np.vstack(pts), np.array(far)
+
+
+def _excess(got, want, prec):
+    """|got - want| / bound per row (<= 1 passes; equal specials -> 0)."""
+    rel, ab = TOL[prec]
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    with np.errstate(invalid="ignore"):
+        r = np.abs(got - want) / np.maximum(rel * np.abs(want), ab)
+    same = (np.isnan(got) & np.isnan(want)) | ((got == want) & np.isinf(want))
+    return np.where(same, 0.0, np.nan_to_num(r, nan=np.inf))
 
 
 @pytest.mark.parametrize("dim,seed", [(10, 1), (30, 7), (50, 3), (100, 11)])
@@ -66,22 +79,27 @@ def test_sweep_random_and_special_points(dim, seed):
     eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=4096, seed=seed))
     orc = Oracle(dim, seed)
     x = np.random.default_rng(seed).uniform(-100, 100, (64, dim))
-    bad = []
+    bad, report = [], []
     for fn in eng.enabled_ids:
-        sp, ill = _special_points(fn, dim, seed)
+        sp, far = _special_points(fn, dim, seed)
         pts = np.vstack([x, sp])
-        ill = np.concatenate([np.zeros(len(x), bool), ill])
+        far = np.concatenate([np.zeros(len(x), bool), far])
         for prec in ("double", "single"):
             got = eng.evaluate(fn, pts, precision=prec).values
             want = orc.evaluate(fn, pts, prec)
-            ok = _close(got, want, prec)
-            if prec == "double":
+            ex = _excess(got, want, prec)
+            near = ex[~far]
+            report.append(f"D={dim} fn={fn:2d} {prec:6s} worst/bar in-box {near.max():.3g}"
+                          f"  far {ex[far].max():.3g}")
+            ok = ex <= 1.0
+            if prec == "double":       # |x| ~ 1e6 rows: 1e-8 relative (module docstring)
                 w = np.asarray(want, dtype=np.float64)
-                ok |= ill & (np.abs(np.asarray(got) - w) <= 1e-8 * np.abs(w))
+                ok |= far & (np.abs(np.asarray(got, dtype=np.float64) - w) <= 1e-8 * np.abs(w))
             if not ok.all():
                 i = int(np.flatnonzero(~ok)[0])
-                bad.append((fn, prec, i, float(got[i]), float(want[i])))
+                bad.append((fn, prec, i, bool(far[i]), float(got[i]), float(want[i])))
     eng.dispose()
+    print("\n".join(report))
     assert not bad, bad[:10]
 
 
