@@ -9,9 +9,13 @@ streams X from HBM).  value = 37 * 2 * N * steps / time, whole job.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun): rows are sharded (dist.Shard, strong scaling: N fixed),
-each rank evaluates its rows and the fitness vector is all-gathered over
-NCCL inside the timed step; time = max over ranks.
+Multi-GPU: one process per GPU.  ``--gpus N`` without a torchrun environment
+re-launches itself under ``torch.distributed.run`` with N ranks.  Rows are
+sharded (dist.Shard, strong scaling: N fixed); each rank queues its rows'
+evaluations without a host synchronisation per call
+(Engine.evaluate_async) and the NCCL all-gather of each function's fitness
+runs on a communication stream, overlapped with the next function's
+evaluation (dist.ShardedEngine.submit); time = max over ranks.
 
 Keys beyond the base contract:
   e2e           same metric through the public API with the population in
@@ -49,6 +53,27 @@ UNIT = "evals/s"
 PREC = ("double", "single")
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> None:
+    """--gpus N > 1 outside torchrun: re-run this command as N ranks (the
+    driver's own launch form: torch.distributed.run, 127.0.0.1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), str(Path(__file__).resolve())]
+    # the ranks read this command's arguments from the environment (torchrun's
+    # own parser would take options such as --n for abbreviations of its own)
+    env = dict(os.environ, RB_BENCH_ARGV=json.dumps(sys.argv[1:]))
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -63,7 +88,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=32, help="rows per process per (fn, precision)")
     ap.add_argument("--breakdown", default="", help="write per-(fn, precision) timings here")
-    return ap.parse_args()
+    argv = json.loads(os.environ["RB_BENCH_ARGV"]) if "RB_BENCH_ARGV" in os.environ else None
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------- helpers
@@ -238,11 +264,14 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1407_7737_b200 import EngineConfig, _lib, initialize
-    from paper_1407_7737_b200.dist import Shard, gather_fitness
+    from paper_1407_7737_b200.dist import Shard, ShardedEngine
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: --gpus {world} needs {world} GPUs, "
+                         f"{torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -268,23 +297,44 @@ def run_ours(args):
                             device=local, dtypes=("double", "single"))
     x64, x32 = xs["double"], xs["single"]
     stream = torch.cuda.current_stream()
+    sharded = ShardedEngine(engine, shard)
+    dts = {"double": torch.float64, "single": torch.float32}
+    # two result slots per precision, reused every other function: the local
+    # values and (N > 1 GPUs) the gathered N-vector; slot k % 2 is rewritten
+    # only after function k's all-gather has finished (its Pending.done)
+    local_bufs = {p: [torch.empty(shard.count, dtype=dts[p], device=dev) for _ in range(2)] for p in precs}
+    full_bufs = ({p: [torch.empty(args.n, dtype=dts[p], device=dev) for _ in range(2)] for p in precs}
+                 if world > 1 else None)
 
     per = {}
 
     def step(record):
+        """All functions x precisions queued back to back: no host
+        synchronisation per call; statuses checked once at the end."""
+        pend = []
         for p in precs:
             for fn in fns:
+                k = len(pend)
+                if k >= 2:
+                    stream.wait_event(pend[k - 2].done)
                 if record:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                local_f = engine.evaluate(fn, xs[p], p).values
+                pend.append(sharded.submit(fn, xs[p], p, local_out=local_bufs[p][k % 2],
+                                           out=full_bufs[p][k % 2] if full_bufs else None))
                 if record:
                     e1.record(stream)
                     per.setdefault((fn, p), []).append((e0, e1))
-                gather_fitness(local_f, shard)
+        for pd in pend:                  # the comm stream's tail joins the step
+            stream.wait_event(pd.done)
+        return pend
+
+    def check(pend):
+        for pd in pend:
+            pd.result()
 
     for _ in range(args.warmup):
-        step(False)
+        check(step(False))
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -293,10 +343,11 @@ def run_ours(args):
     launches0 = _lib.launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for _ in range(args.steps):
-        step(True)
+    pends = [step(True) for _ in range(args.steps)]
     t_end.record(stream)
     torch.cuda.synchronize()
+    for pd in pends:
+        check(pd)
     barrier()
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
@@ -364,18 +415,29 @@ def run_ours(args):
         d2h = 0
 
         def e2e_step_plain():
+            # N > 1 GPUs: this rank's rows in, every function's full N-vector
+            # (after the all-gather) out, evaluations queued without a host
+            # synchronisation per call (dist.ShardedEngine.submit)
             nonlocal d2h
             d2h = 0
             dev_x.copy_(host_x, non_blocking=True)
             x32e = dev_x.float()
+            pend = []
             for p in precs:
                 xe = dev_x if p == "double" else x32e
                 for fn in fns:
-                    full = gather_fitness(engine.evaluate(fn, xe, p).values, shard)
+                    k = len(pend)
+                    if k >= 2:
+                        stream.wait_event(pend[k - 2].done)
+                    pd = sharded.submit(fn, xe, p, local_out=local_bufs[p][k % 2], out=full_bufs[p][k % 2])
+                    stream.wait_event(pd.done)
+                    full = pd.values
                     dst = host_f[: full.numel()] if p == "double" else host_f.view(torch.float32)[: full.numel()]
                     dst.copy_(full, non_blocking=True)
                     d2h += full.numel() * full.element_size()
+                    pend.append(pd)
             torch.cuda.synchronize()
+            check(pend)
 
         # one GPU: a chunked pipeline -- the H2D copy of row chunk c+1 and the
         # D2H of chunk c-1's fitness values run on a copy stream while chunk c
@@ -414,6 +476,7 @@ def run_ours(args):
                     lo_, hi_ = bounds[c], bounds[c + 1]
                     dev_x[lo_:hi_].copy_(host_x[lo_:hi_], non_blocking=True)
                     ev_in[c].record(copy_stream)
+            pend = []
             for c in range(n_chunks):
                 lo_, hi_ = bounds[c], bounds[c + 1]
                 nc = hi_ - lo_
@@ -424,7 +487,8 @@ def run_ours(args):
                 xcs = {"double": xc, "single": xc.float()}
                 for p in precs:
                     for i, fn in enumerate(fns):
-                        engine.evaluate(fn, xcs[p], p, out=res[p][c % 2, i * nc:(i + 1) * nc])
+                        pend.append(engine.evaluate_async(fn, xcs[p], p,
+                                                          out=res[p][c % 2, i * nc:(i + 1) * nc]))
                 ev_done[c].record(stream)
                 with torch.cuda.stream(out_stream):
                     out_stream.wait_event(ev_done[c])
@@ -436,6 +500,7 @@ def run_ours(args):
             stream.wait_stream(copy_stream)
             stream.wait_stream(out_stream)
             torch.cuda.synchronize()
+            check(pend)
 
         e2e_step = e2e_step_pipelined if world == 1 else e2e_step_plain
 
@@ -458,7 +523,7 @@ def run_ours(args):
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
                "pipeline": (f"{n_chunks} row chunks (small first and last ones): H2D of X and D2H of every fitness vector on two "
                             "copy streams, overlapped with evaluation" if world == 1 else
-                            "H2D, evaluate + NCCL all-gather, D2H per function")}
+                            "H2D, evaluations queued with their NCCL all-gathers overlapped, D2H per function")}
         del host_x, host_f, host_res, res
 
     cpu = None
@@ -495,6 +560,7 @@ def run_ours(args):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         run_reference(args)
     else:

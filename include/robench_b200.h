@@ -139,6 +139,46 @@ rb_status rb_h_func_evaluate (rb_engine* e, int32_t fn_id, const double* x, int6
 rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n,
                               float* f);
 
+/* ---- stream-ordered calls with a deferred status ------------------------ */
+/* precision: RB_DOUBLE (x, f are double*) or RB_SINGLE (float*). */
+#define RB_DOUBLE 0
+#define RB_SINGLE 1
+/* Enqueue the evaluation on `stream` and return at once: argument errors
+ * (the reference's validation order) come back now; the input's finiteness
+ * (NonFiniteInput) is read later with rb_ticket_status, after the caller has
+ * synchronised `stream` (or an event recorded after this call).  At most
+ * 4096 calls per engine may be outstanding.  Lets a caller queue many
+ * functions, and overlap them with copies or collectives, without a host
+ * synchronisation per call (the blocking rb_func_evaluate[f] wait on the
+ * stream to read the status). */
+rb_status rb_func_evaluate_async(rb_engine* e, int32_t fn_id, int32_t precision, const void* x,
+                                 int64_t n, void* f, void* stream, int64_t* ticket);
+/* RB_OK or RB_E_NON_FINITE_INPUT for a completed call; RB_E_INVALID_ARGUMENT
+ * once the ticket's slot was reused (4096 later calls). */
+rb_status rb_ticket_status(rb_engine* e, int64_t ticket);
+
+/* ---- one process, several GPUs ---------------------------
+ * A replica of the instance pack on each device; rows are sharded
+ * contiguously, device g owning rows [start_g, start_g + count_g) with
+ * count_g = n/G (+1 for the first n%G devices).  x_shards[g]: device g's rows
+ * (row-major count_g x dim, on devices[g]); f_full[g]: a length-n_total buffer
+ * on devices[g].  Each device evaluates its rows into f_full[g] + start_g and
+ * stores that slice into every peer's f_full (P2P stores over NVLink /
+ * NVSwitch; copy-engine peer copies where peer access is unavailable), so on
+ * completion every f_full[g] holds all n_total values -- the fitness
+ * all-gather.  streams: per-device cudaStream_t, a NULL entry being that
+ * device's legacy default stream; a NULL array: the engine's own streams.  tickets == NULL: synchronous, errors as rb_func_evaluate;
+ * else tickets[g] receives device g's ticket (-1: no rows) and the call
+ * returns once everything is queued (rb_sharded_ticket_status). */
+typedef struct rb_sharded rb_sharded;
+rb_status rb_initialize_sharded(const rb_pack* pack, int64_t max_concurrency_per_device,
+                                const int32_t* devices, int32_t n_devices, rb_sharded** out);
+rb_status rb_func_evaluate_sharded(rb_sharded* s, int32_t fn_id, int32_t precision,
+                                   const void* const* x_shards, int64_t n_total, void* const* f_full,
+                                   void* const* streams, int64_t* tickets);
+rb_status rb_sharded_ticket_status(rb_sharded* s, int32_t device_index, int64_t ticket);
+rb_status rb_dispose_sharded(rb_sharded** s);      /* idempotent; *s = NULL */
+
 /* ---- introspection ---------------------------------------------------- */
 const char* rb_last_error(void);                   /* thread-local message */
 int32_t rb_abi_version(void);

@@ -75,6 +75,24 @@ __global__ void uniform_population_kernel(uint64_t k0, uint64_t k1, uint64_t fir
   }
 }
 
+// The fitness all-gather of the single-process multi-device path
+// (rb_func_evaluate_sharded): one device's slice of f stored into every
+// peer's full-length f over NVLink (P2P stores; peers' slices are disjoint).
+constexpr int kMaxDevices = 16;
+struct PeerDst {
+  void* p[kMaxDevices];
+  int n;
+};
+
+template <class T>
+__global__ void peer_scatter_kernel(const T* __restrict__ src, int64_t n, PeerDst dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = src[i];
+    for (int k = 0; k < dst.n; ++k) static_cast<T*>(dst.p[k])[i] = v;
+  }
+}
+
 __global__ void np_powf_kernel(const float* x, const float* y, float* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -87,6 +105,7 @@ namespace {
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
 constexpr uint32_t kFlagSlots = 4096;      // a power of two: slot = counter & (kFlagSlots - 1)
+constexpr int kSlotInts = 4;               // [0] non-finite, [1] rows left for fixup, [2] call number
 static_assert((kFlagSlots & (kFlagSlots - 1)) == 0, "flag ring must be a power of two");
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per (device,
@@ -184,6 +203,16 @@ struct rb_engine {
   cudaStream_t host_stream = nullptr;
 };
 
+// A replica of the engine on each of several devices:
+// rows are sharded contiguously, each device evaluates its rows into its own
+// full-length f and stores that slice into every peer's f (peer_scatter).
+struct rb_sharded {
+  std::vector<rb_engine*> eng;
+  std::vector<int> dev;
+  std::vector<cudaStream_t> streams;         // used when the caller passes none
+  bool p2p = true;                           // every distinct pair has peer access
+};
+
 namespace {
 
 void release(rb_engine* e) {
@@ -257,7 +286,8 @@ rb_status launch_fixup(rb_engine* e, int32_t fn_id, const double* x, int64_t n, 
 // the kernel (callers that do not inspect the flags before using f).
 template <class T>
 rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
-                      cudaStream_t stream, volatile int** flag_out, bool fixup_now = false) {
+                      cudaStream_t stream, volatile int** flag_out, bool fixup_now = false,
+                      uint32_t* seq_out = nullptr) {
   // validation in the reference's order (engine.py:180-203)
   if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
   if (fn_id < 0 || fn_id >= (int32_t)e->fns.size())
@@ -273,15 +303,18 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
     return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fn_id) + ": " + e->why[pi][fn_id]);
   const Launch& L = e->launch[pi][fn_id];
 
-  const uint32_t slot = e->next_flag.fetch_add(1) & (kFlagSlots - 1);
+  const uint32_t seq = e->next_flag.fetch_add(1);
+  const uint32_t slot = seq & (kFlagSlots - 1);
+  if (seq_out) *seq_out = seq;
   // the flags live in mapped pinned memory: cleared by the host, set by the
   // kernel with a plain store over PCIe, read after the stream sync (no
   // memset / D2H copy that would queue behind bulk transfers on the copy
   // engines)
-  volatile int* hflag = e->h_flags + 2 * slot;      // [0] non-finite, [1] rows left for fixup
+  volatile int* hflag = e->h_flags + kSlotInts * slot;
   hflag[0] = 0;
   hflag[1] = 0;
-  int* dflag = e->d_flags + 2 * slot;
+  hflag[2] = (int)seq;
+  int* dflag = e->d_flags + kSlotInts * slot;
 
   rb::Args<T> a = make_args<T>(e, fn_id, x, n, f, dflag, L);
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
@@ -636,6 +669,96 @@ rb_status upload_series_constants(const rb_pack* pk) {
   return RB_OK;
 }
 
+// Stream-ordered call: validation now, the status later (rb_ticket_status).
+// float64 functions with exact64 members queue their fixup pass behind the
+// kernel, since nobody inspects the flags in between.
+template <class T>
+rb_status evaluate_async(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
+                         cudaStream_t stream, int64_t* ticket) {
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
+  volatile int* flag = nullptr;
+  uint32_t seq = 0;
+  const rb_status s = launch_eval<T>(e, fn_id, x, n, f, stream, &flag, true, &seq);
+  if (s == RB_OK && ticket) *ticket = (int64_t)seq;
+  if (prev != e->device) cudaSetDevice(prev);
+  return s;
+}
+
+rb_status ticket_status(rb_engine* e, int64_t ticket) {
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (ticket < 0) return fail(RB_E_INVALID_ARGUMENT, "bad ticket");
+  const uint32_t seq = (uint32_t)ticket;
+  const volatile int* hf = e->h_flags + kSlotInts * (seq & (kFlagSlots - 1));
+  if ((uint32_t)hf[2] != seq)
+    return fail(RB_E_INVALID_ARGUMENT, "ticket expired: more than 4096 calls issued since");
+  return hf[0] ? non_finite() : RB_OK;
+}
+
+template <class T>
+rb_status evaluate_sharded(rb_sharded* sh, int32_t fn_id, const void* const* x_shards, int64_t n_total,
+                           void* const* f_full, void* const* streams, int64_t* tickets) {
+  const int G = (int)sh->eng.size();
+  if (n_total < 1 || !x_shards || !f_full) return fail(RB_E_INVALID_ARGUMENT, "empty batch or null pointer");
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  const int64_t base = n_total / G, extra = n_total % G;
+  std::vector<int64_t> start(G + 1, 0);
+  for (int g = 0; g < G; ++g) start[g + 1] = start[g] + base + (g < extra ? 1 : 0);
+  std::vector<volatile int*> flags(G, nullptr);
+  rb_status st = RB_OK;
+  for (int g = 0; g < G && st == RB_OK; ++g) {
+    const int64_t cnt = start[g + 1] - start[g];
+    if (tickets) tickets[g] = -1;
+    if (cnt == 0) continue;                  // fewer rows than devices
+    cudaStream_t stream = streams ? static_cast<cudaStream_t>(streams[g]) : sh->streams[g];
+    if (cudaSetDevice(sh->dev[g]) != cudaSuccess) {
+      st = fail(RB_E_CUDA, "cudaSetDevice failed");
+      break;
+    }
+    T* fg = static_cast<T*>(f_full[g]) + start[g];
+    uint32_t seq = 0;
+    st = launch_eval<T>(sh->eng[g], fn_id, static_cast<const T*>(x_shards[g]), cnt, fg, stream,
+                        &flags[g], true, &seq);
+    if (st != RB_OK) break;
+    if (tickets) tickets[g] = (int64_t)seq;
+    if (G == 1) continue;
+    if (sh->p2p) {                           // this slice into every peer's f, over NVLink
+      rb::PeerDst dst{};
+      for (int h = 0; h < G; ++h)
+        if (h != g) dst.p[dst.n++] = static_cast<T*>(f_full[h]) + start[g];
+      const int grid = (int)std::min<int64_t>((cnt + 255) / 256, 148 * 4);
+      rb::peer_scatter_kernel<T><<<grid, 256, 0, stream>>>(fg, cnt, dst);
+      g_launches.fetch_add(1);
+      const cudaError_t err = cudaGetLastError();
+      if (err != cudaSuccess) st = fail(RB_E_CUDA, std::string("peer_scatter: ") + cudaGetErrorString(err));
+    } else {                                 // no peer access: copy-engine copies
+      for (int h = 0; h < G && st == RB_OK; ++h) {
+        if (h == g) continue;
+        const cudaError_t err = cudaMemcpyPeerAsync(static_cast<T*>(f_full[h]) + start[g], sh->dev[h], fg,
+                                                    sh->dev[g], sizeof(T) * cnt, stream);
+        if (err != cudaSuccess) st = fail(RB_E_CUDA, std::string("cudaMemcpyPeerAsync: ") + cudaGetErrorString(err));
+      }
+    }
+  }
+  if (st == RB_OK && !tickets) {             // synchronous: wait, then the reference's errors
+    for (int g = 0; g < G; ++g) {
+      if (!flags[g]) continue;
+      cudaStream_t stream = streams ? static_cast<cudaStream_t>(streams[g]) : sh->streams[g];
+      cudaSetDevice(sh->dev[g]);
+      const cudaError_t err = cudaStreamSynchronize(stream);
+      if (err != cudaSuccess && st == RB_OK)
+        st = fail(RB_E_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(err));
+    }
+    for (int g = 0; g < G && st == RB_OK; ++g)
+      if (flags[g] && flags[g][0]) st = non_finite();
+  }
+  cudaSetDevice(prev);
+  return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -708,7 +831,7 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   if (s == RB_OK) s = upload(&e->d_index, pk->index, pk->n_index);
   if (s == RB_OK) s = upload(&e->d_v64, pk->values_f64, pk->n_values);
   if (s == RB_OK) s = upload(&e->d_v32, pk->values_f32, pk->n_values);
-  if (s == RB_OK && cudaHostAlloc(reinterpret_cast<void**>(&e->h_flags), 2 * sizeof(int) * kFlagSlots,
+  if (s == RB_OK && cudaHostAlloc(reinterpret_cast<void**>(&e->h_flags), kSlotInts * sizeof(int) * kFlagSlots,
                                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
     s = fail(RB_E_CUDA, "mapped flag allocation failed");
   if (s == RB_OK && cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_flags), e->h_flags, 0) !=
@@ -748,6 +871,99 @@ rb_status rb_h_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64
 
 rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f) {
   return evaluate_host<float>(e, fn_id, x, n, f);
+}
+
+rb_status rb_func_evaluate_async(rb_engine* e, int32_t fn_id, int32_t precision, const void* x,
+                                 int64_t n, void* f, void* stream, int64_t* ticket) {
+  if (precision == RB_DOUBLE)
+    return evaluate_async<double>(e, fn_id, static_cast<const double*>(x), n, static_cast<double*>(f),
+                                  static_cast<cudaStream_t>(stream), ticket);
+  if (precision == RB_SINGLE)
+    return evaluate_async<float>(e, fn_id, static_cast<const float*>(x), n, static_cast<float*>(f),
+                                 static_cast<cudaStream_t>(stream), ticket);
+  return fail(RB_E_INVALID_ARGUMENT, "precision must be RB_DOUBLE or RB_SINGLE");
+}
+
+rb_status rb_ticket_status(rb_engine* e, int64_t ticket) { return ticket_status(e, ticket); }
+
+rb_status rb_initialize_sharded(const rb_pack* pk, int64_t max_concurrency, const int32_t* devices,
+                                int32_t n_devices, rb_sharded** out) {
+  if (!out) return fail(RB_E_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  if (!devices || n_devices < 1 || n_devices > rb::kMaxDevices)
+    return fail(RB_E_INVALID_ARGUMENT, "1..16 devices required");
+  rb_sharded* sh = new rb_sharded();
+  int prev = 0;
+  cudaGetDevice(&prev);
+  rb_status st = RB_OK;
+  for (int g = 0; g < n_devices && st == RB_OK; ++g) {
+    rb_engine* e = nullptr;
+    st = rb_initialize(pk, max_concurrency, devices[g], &e);
+    if (st != RB_OK) break;
+    sh->eng.push_back(e);
+    sh->dev.push_back(devices[g]);
+    cudaStream_t s = nullptr;
+    cudaSetDevice(devices[g]);
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+      st = fail(RB_E_CUDA, "stream creation failed");
+    sh->streams.push_back(s);
+  }
+  // peer access for the P2P all-gather stores (NVLink / NVSwitch)
+  for (int g = 0; g < n_devices && st == RB_OK; ++g)
+    for (int h = 0; h < n_devices; ++h) {
+      if (devices[g] == devices[h]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[g], devices[h]);
+      if (!can) {
+        sh->p2p = false;
+        continue;
+      }
+      cudaSetDevice(devices[g]);
+      const cudaError_t err = cudaDeviceEnablePeerAccess(devices[h], 0);
+      if (err == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (err != cudaSuccess) sh->p2p = false;
+    }
+  cudaSetDevice(prev);
+  if (st != RB_OK) {
+    rb_dispose_sharded(&sh);
+    return st;
+  }
+  *out = sh;
+  return RB_OK;
+}
+
+rb_status rb_dispose_sharded(rb_sharded** sh) {
+  if (!sh || !*sh) return RB_OK;
+  rb_sharded* s = *sh;
+  for (size_t g = 0; g < s->eng.size(); ++g) {
+    if (g < s->streams.size() && s->streams[g]) {
+      cudaSetDevice(s->dev[g]);
+      cudaStreamDestroy(s->streams[g]);
+    }
+    rb_dispose(&s->eng[g]);
+  }
+  delete s;
+  *sh = nullptr;
+  return RB_OK;
+}
+
+rb_status rb_func_evaluate_sharded(rb_sharded* sh, int32_t fn_id, int32_t precision,
+                                   const void* const* x_shards, int64_t n_total, void* const* f_full,
+                                   void* const* streams, int64_t* tickets) {
+  if (!sh) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (precision == RB_DOUBLE)
+    return evaluate_sharded<double>(sh, fn_id, x_shards, n_total, f_full, streams, tickets);
+  if (precision == RB_SINGLE)
+    return evaluate_sharded<float>(sh, fn_id, x_shards, n_total, f_full, streams, tickets);
+  return fail(RB_E_INVALID_ARGUMENT, "precision must be RB_DOUBLE or RB_SINGLE");
+}
+
+rb_status rb_sharded_ticket_status(rb_sharded* sh, int32_t device_index, int64_t ticket) {
+  if (!sh) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (device_index < 0 || device_index >= (int32_t)sh->eng.size())
+    return fail(RB_E_INVALID_ARGUMENT, "device index out of range");
+  if (ticket == -1) return RB_OK;            // that device had no rows
+  return ticket_status(sh->eng[device_index], ticket);
 }
 
 rb_status rb_uniform_population(uint64_t key0, uint64_t key1, uint64_t first_element,

@@ -171,6 +171,49 @@ class Engine:
             raise ValueError("out= is only supported for CUDA tensor batches")
         return EvalResult(self._evaluate_host(fn_id, batch.data, precision))
 
+    def evaluate_async(self, fn_id: int, batch, precision: str | None = None, *,
+                       out=None) -> "Pending":
+        """Queue the evaluation of a CUDA-tensor batch on the current stream
+        and return at once (rb_func_evaluate_async): argument errors are
+        raised now, in the reference's order; NonFiniteInput is raised by
+        ``Pending.result()``, which waits for the values.  No host
+        synchronisation per call, so callers can overlap many functions with
+        copies or collectives (dist.ShardedEngine, bench.py)."""
+        import torch
+        if self._disposed:
+            raise UseAfterDispose("engine was disposed")
+        if not isinstance(batch, PointBatch):
+            batch = PointBatch(batch)
+        if not _is_torch(batch.data):
+            raise ValueError("evaluate_async takes CUDA tensor batches (host arrays: evaluate)")
+        catalog.lookup(fn_id)
+        fn_id = int(fn_id)
+        if fn_id in self._disabled:
+            raise DisabledFunction(
+                f"function {fn_id} needs dimension >= {catalog.MIN_CONSTRUCTED_DIMENSION}")
+        if batch.count > self.config.max_concurrency:
+            raise BatchTooLarge(f"batch of {batch.count} exceeds "
+                                f"max_concurrency={self.config.max_concurrency}")
+        if batch.dim != self.config.dim:
+            raise DimensionMismatch(f"batch dim {batch.dim} != engine dim {self.config.dim}")
+        precision = precision or self.config.precision
+        if precision not in _DTYPES:
+            raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
+        pts, out = self._device_args(batch.data, precision, out)
+        stream = torch.cuda.current_stream(pts.device)
+        ticket = ctypes.c_int64(-1)
+        _lib.check(_lib.load().rb_func_evaluate_async(
+            self._handle, fn_id, _lib.RB_DOUBLE if precision == "double" else _lib.RB_SINGLE,
+            pts.data_ptr(), pts.shape[0], out.data_ptr(), stream.cuda_stream, ctypes.byref(ticket)))
+        done = torch.cuda.Event()
+        done.record(stream)
+        return Pending(out, [(self, ticket.value)], done, keep=(pts,))
+
+    def ticket_status(self, ticket: int) -> None:
+        """Raise NonFiniteInput if the completed call behind ``ticket`` saw a
+        non-finite input (rb_ticket_status)."""
+        _lib.check(_lib.load().rb_ticket_status(self._handle, int(ticket)))
+
     def evaluate_single_precision(self, fn_id: int, batch) -> EvalResult:
         return self.evaluate(fn_id, batch, precision="single")
 
@@ -197,7 +240,7 @@ class Engine:
         _lib.check(call(self._handle, fn_id, _lib.ptr(pts), pts.shape[0], _lib.ptr(out)))
         return out
 
-    def _evaluate_device(self, fn_id, data, precision, out=None):
+    def _device_args(self, data, precision, out):
         import torch
         if not data.is_cuda or data.device.index != self.config.device:
             raise ValueError(f"tensor must live on cuda:{self.config.device}")
@@ -208,10 +251,32 @@ class Engine:
         elif (out.dtype != dt or out.device != pts.device or not out.is_contiguous()
               or out.numel() != pts.shape[0]):
             raise ValueError("out must be a contiguous device tensor of the batch's length and dtype")
+        return pts, out
+
+    def _evaluate_device(self, fn_id, data, precision, out=None):
+        import torch
+        pts, out = self._device_args(data, precision, out)
         stream = torch.cuda.current_stream(pts.device).cuda_stream
-        call = _lib.load().rb_func_evaluate if dt == torch.float64 else _lib.load().rb_func_evaluatef
+        call = _lib.load().rb_func_evaluate if pts.dtype == torch.float64 else _lib.load().rb_func_evaluatef
         _lib.check(call(self._handle, fn_id, pts.data_ptr(), pts.shape[0], out.data_ptr(), stream))
         return out
+
+
+class Pending:
+    """An evaluation queued on a stream (Engine.evaluate_async,
+    dist.ShardedEngine.submit): ``values`` fills in once ``done`` completes;
+    ``result()`` waits for it and raises the reference's NonFiniteInput if
+    any contributing call saw a non-finite input."""
+
+    def __init__(self, values, tickets, done, keep=()):
+        self.values, self._tickets, self.done, self._keep = values, tickets, done, keep
+
+    def result(self) -> EvalResult:
+        self.done.synchronize()
+        for eng, ticket in self._tickets:
+            eng.ticket_status(ticket)
+        self._keep = ()
+        return EvalResult(self.values)
 
 
 class _PointEvaluator:

@@ -42,7 +42,7 @@ def _worker(rank, world, port, n, out):
     eng = ShardedEngine(OracleEngine(10), sh)
     local = torch.from_numpy(x[sh.start:sh.start + sh.count])
     for fn in (0, 23, 30):
-        full = eng.evaluate(fn, local, "double")
+        full = eng.evaluate(fn, local, "double").values
         if rank == 0:
             np.save(f"{out}_{fn}.npy", full.numpy())
     dist.destroy_process_group()
