@@ -25,7 +25,7 @@ Keys beyond the base contract:
                 T_roof = max(N*(D+1)*s / HBM, N*F / P_fp),
                 F = 2*nnz of the rotations applied; P_fp = measured DMMA fp64
                 (fp64) or exact-order FMUL+FADD (fp32) peak on this pool
-                (profiles/peaks_r01.json), HBM from MEASURED_PEAKS.json.
+                (profiles/r02/peaks.json), HBM from MEASURED_PEAKS.json.
   cpu_baseline  the reference path (CPU oracle port, per-point NumPy loop as
                 engine.py:205-209) timed on a bounded row sample on all host
                 cores, rank 0, N=1 only.
@@ -86,10 +86,41 @@ def parse():
     ap.add_argument("--precisions", default="double,single")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=32, help="rows per process per (fn, precision)")
+    ap.add_argument("--cpu-rows", type=int, default=20000,
+                    help="cpu_baseline: rows in the all-core sample, min(N, this) (BASELINE.md section 2)")
+    ap.add_argument("--cpu-rows-1core", type=int, default=400,
+                    help="cpu_baseline: rows timed on one pinned core")
+    ap.add_argument("--ref-rows", type=int, default=2048,
+                    help="--impl reference: rows per step (all cores)")
     ap.add_argument("--breakdown", default="", help="write per-(fn, precision) timings here")
+    ap.add_argument("--config", type=int, default=5, choices=(1, 2, 3, 4, 5),
+                    help="BASELINE.json config (SURVEY.md 8d): 1 sphere D=10 N=1e3 fp64 (latency); "
+                         "2 ids 0-22 D=30 N=1e5; 3 ids 23-28 D=50 N=1e6; 4 ids 29-36 D=100 N=1e6 "
+                         "fp64; 5 (default) all 37 D=100 N=1e7")
+    ap.add_argument("--e2e-numpy", action="store_true",
+                    help="config 5: also time the NumPy host-array path (74 x 8/4 GB H2D per step)")
     argv = json.loads(os.environ["RB_BENCH_ARGV"]) if "RB_BENCH_ARGV" in os.environ else None
-    return ap.parse_args(argv)
+    args = ap.parse_args(argv)
+    preset = CONFIGS[args.config]
+    if args.config != 5:
+        args.dim, args.n, args.fns, args.precisions = (preset["dim"], preset["n"], preset["fns"],
+                                                       preset["precisions"])
+    return args
+
+
+# BASELINE.json "configs" as SURVEY.md 8d fixes them
+CONFIGS = {
+    1: {"dim": 10, "n": 1000, "fns": "0", "precisions": "double",
+        "name": "shifted-rotated Sphere (f1) D=10, N=1,000 random points, FP64 (latency)"},
+    2: {"dim": 30, "n": 100_000, "fns": ",".join(map(str, range(23))), "precisions": "double,single",
+        "name": "all basic functions shifted+rotated at D=30, N=100,000, FP64 and FP32"},
+    3: {"dim": 50, "n": 1_000_000, "fns": ",".join(map(str, range(23, 29))), "precisions": "double,single",
+        "name": "hybrid functions at D=50, N=1,000,000, FP64 and FP32"},
+    4: {"dim": 100, "n": 1_000_000, "fns": ",".join(map(str, range(29, 37))), "precisions": "double",
+        "name": "composition functions at D=100, N=1,000,000, FP64"},
+    5: {"dim": 100, "n": 10_000_000, "fns": "all", "precisions": "double,single",
+        "name": "full suite at D=100, N=10^7 (sharded across the GPUs)"},
+}
 
 
 # ----------------------------------------------------------------- helpers
@@ -107,8 +138,8 @@ def ncu_pipes(fn, prec):
     its latest committed ncu --set full summary (profiles/r01/v*/), or None:
     the transcendental work the rotate-flop roofline leaves out."""
     import glob
-    cands = sorted(glob.glob(str(ROOT / "profiles" / "r01" / "v*" / f"ncu_full_fn{fn}_{prec}.txt")),
-                   key=lambda p: int(Path(p).parent.name[1:]))
+    cands = sorted(glob.glob(str(ROOT / "profiles" / "r0[12]" / "v*" / f"ncu_full_fn{fn}_{prec}.txt")),
+                   key=lambda p: (Path(p).parent.parent.name, int(Path(p).parent.name[1:])))
     if not cands:
         return None
     vals = {}
@@ -191,8 +222,13 @@ def rotate_flops(pack, fn: int) -> int:
 
 # ------------------------------------------------------------ CPU baseline
 def _cpu_worker(job):
-    dim, fns, precs, rows = job
+    dim, fns, precs, rows, core = job
     sys.path.insert(0, str(ROOT))
+    if core is not None:
+        try:
+            os.sched_setaffinity(0, {core})
+        except (AttributeError, OSError):
+            pass
     from oracle.robench_oracle import Oracle
     orc = Oracle(dim, 0)
     for fn in fns:                      # build outside the timed loop (initialize)
@@ -207,17 +243,18 @@ def _cpu_worker(job):
     return n, time.perf_counter() - t0
 
 
-def cpu_reference(dim, fns, precs, rows_per_proc, x_rows=None, procs=None, n_total=None):
+def cpu_reference(dim, fns, precs, rows_per_proc, x_rows=None, procs=None, n_total=None,
+                  pin: bool = False):
     """The reference's per-point path (oracle port, bit-identical to
     robench) on every host core: P processes over disjoint row slices of the
-    first rows of the §8d population."""
+    first rows of the §8d population (pin: process i on core i)."""
     import multiprocessing as mp
     procs = procs or os.cpu_count() or 1
     if x_rows is None:
         from paper_1407_7737_b200.population import host_rows, workload_entropy
         x_rows = host_rows(dim, workload_entropy(dim, n_total or rows_per_proc * procs), 0,
                            rows_per_proc * procs)
-    jobs = [(dim, fns, precs, x_rows[i * rows_per_proc:(i + 1) * rows_per_proc])
+    jobs = [(dim, fns, precs, x_rows[i * rows_per_proc:(i + 1) * rows_per_proc], i if pin else None)
             for i in range(procs)]
     ctx = mp.get_context("fork")
     with ctx.Pool(procs) as pool:
@@ -237,9 +274,11 @@ def run_reference(args):
         return
     fns = list(range(37)) if args.fns == "all" else [int(f) for f in args.fns.split(",")]
     precs = [p for p in args.precisions.split(",")]
+    procs = os.cpu_count() or 1
+    per_proc = max(1, -(-min(args.ref_rows, args.n) // procs))
     for _ in range(max(args.warmup, 0)):
-        cpu_reference(args.dim, fns, precs, max(2, args.cpu_rows // 8), n_total=args.n)
-    vals = [cpu_reference(args.dim, fns, precs, args.cpu_rows, n_total=args.n) for _ in range(args.steps)]
+        cpu_reference(args.dim, fns, precs, max(1, per_proc // 8), n_total=args.n)
+    vals = [cpu_reference(args.dim, fns, precs, per_proc, n_total=args.n) for _ in range(args.steps)]
     cores = vals[0]["cores"]
     value = statistics.median(v["value"] for v in vals)
     line = {
@@ -298,6 +337,14 @@ def run_ours(args):
     x64, x32 = xs["double"], xs["single"]
     stream = torch.cuda.current_stream()
     sharded = ShardedEngine(engine, shard)
+    # inputs smaller than twice the L2 (configs 1-2): calls cycle through
+    # copies of X whose total exceeds it, so no call reads a warm X
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    xbytes = shard.count * D * 8
+    n_rot = 1 if xbytes >= 2 * l2 else int(min(64, -(-2 * l2 // xbytes)))
+    xrot = [xs] + [{p: t.clone() for p, t in xs.items()} for _ in range(n_rot - 1)]
+    l2_note = ("inputs larger than L2" if n_rot == 1 else
+               f"{n_rot} rotating copies of X ({n_rot * xbytes / 1e6:.0f} MB fp64 > 2 x {l2 / 1e6:.0f} MB L2)")
     dts = {"double": torch.float64, "single": torch.float32}
     # two result slots per precision, reused every other function: the local
     # values and (N > 1 GPUs) the gathered N-vector; slot k % 2 is rewritten
@@ -320,14 +367,18 @@ def run_ours(args):
                 if record:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                pend.append(sharded.submit(fn, xs[p], p, local_out=local_bufs[p][k % 2],
+                xk = xrot[(step.calls + k) % n_rot][p]
+                pend.append(sharded.submit(fn, xk, p, local_out=local_bufs[p][k % 2],
                                            out=full_bufs[p][k % 2] if full_bufs else None))
                 if record:
                     e1.record(stream)
                     per.setdefault((fn, p), []).append((e0, e1))
         for pd in pend:                  # the comm stream's tail joins the step
             stream.wait_event(pd.done)
+        step.calls += len(pend)
         return pend
+
+    step.calls = 0
 
     def check(pend):
         for pd in pend:
@@ -362,10 +413,14 @@ def run_ours(args):
 
     # per-(fn, precision) device time and roofline
     peaks = load_json(ROOT / "MEASURED_PEAKS.json")
-    mypk = load_json(ROOT / "profiles" / "peaks_r01.json")
+    peaks_file = ROOT / "profiles" / "r02" / "peaks.json"      # tools/peaks_microbench.cu
+    mypk = load_json(peaks_file)
     hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    # compute ceilings of the rotate: DMMA f64 for float64;
+    # for float32 the exact-order pair (rounded product + rounded add: two
+    # FP32-pipe instructions per MAC, NumPy's rounding rules out FMA/TF32)
     p_fp = {"double": float(mypk.get("dmma_m16n8k4_tflops", 36.9)) * 1e12,
-            "single": float(mypk.get("fmul_fadd_tflops", 65.5)) * 1e12}
+            "single": float(mypk.get("fmul_fadd_tflops", 36.6)) * 1e12}
     rows = []
     for (fn, p), evs in per.items():
         t = sum(a.elapsed_time(b) for a, b in evs) / 1e3 / len(evs)
@@ -392,8 +447,10 @@ def run_ours(args):
         "kernel": f"rb::evaluate_kernel<{'double' if dom['precision'] == 'double' else 'float'}> "
                   f"fn={dom['fn']}",
         "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if bound == "hbm" else
-                        "profiles/peaks_r01.json (tools/peaks_microbench.cu on this pool: "
-                        + ("DMMA m16n8k4 f64" if dom["precision"] == "double" else "FMUL+FADD f32") + ")"),
+                        "profiles/r02/peaks.json (tools/peaks_microbench.cu on this pool: "
+                        + ("DMMA m16n8k4 f64" if dom["precision"] == "double" else
+                           "FMUL+FADD f32 exact-order pair; FFMA peak %s TF/s beside it"
+                           % mypk.get("ffma_tflops", "?")) + ")"),
         "suite_frac": sum(max(r["t_roof_hbm"], r["t_roof_fp"]) for r in rows) / sum(r["seconds"] for r in rows),
         # the compute bound is the rotation's 2*nnz flops: DMMA (tensor
         # pipe) in fp64; exact-order SIMT FMUL+FADD in fp32 (NumPy's rounding rules out
@@ -404,9 +461,48 @@ def run_ours(args):
         "pipe_utilization": ncu_pipes(dom["fn"], dom["precision"]),
     }
 
-    # e2e through the public API from pinned host memory
+    # e2e through the reference's own call: Engine.evaluate(fn, numpy X,
+    # precision) with X in ordinary (pageable) host memory, values back as
+    # NumPy -> rb_h_func_evaluate[f], H2D of X and D2H of f in every call
+    e2e_numpy = None
+    latency = None
+    if not args.no_e2e and world == 1 and (args.config != 5 or args.e2e_numpy):
+        xh = x64.cpu().numpy()
+        calls = []
+
+        def np_step():
+            for p in precs:
+                for fn in fns:
+                    t0 = time.perf_counter()
+                    engine.evaluate(fn, xh, p)
+                    calls.append(time.perf_counter() - t0)
+
+        np_step()
+        calls.clear()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            np_step()
+        wall = time.perf_counter() - t0
+        h2d = sum(shard.count * D * (8 if p == "double" else 4) for p in precs for _ in fns)
+        d2h = sum(shard.count * (8 if p == "double" else 4) for p in precs for _ in fns)
+        e2e_numpy = {"value": args.steps * len(fns) * len(precs) * args.n / wall, "unit": UNIT,
+                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                     "ms_per_step": 1e3 * wall / args.steps,
+                     "path": ("Engine.evaluate(fn, numpy float64 X, precision) -> rb_h_func_evaluate[f]; "
+                              "float32 calls cast X on the host first, as the reference does (engine.py:201)"),
+                     "timing": "host wall clock around the blocking calls"}
+        if args.config == 1:
+            dev_us = sorted(1e3 * a.elapsed_time(b) for evs in per.values() for a, b in evs)
+            latency = {"device_us_per_call_median": dev_us[len(dev_us) // 2],
+                       "host_blocking_us_per_call_median": 1e6 * statistics.median(calls),
+                       "calls": len(calls),
+                       "note": "device: CUDA events around one evaluation (N=1000 rows); host: the "
+                               "whole blocking NumPy call (validation, H2D, kernel, D2H)"}
+        del xh
+
+    # e2e through the public API from pinned host memory (config 5)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.config == 5:
         host_x = torch.empty((shard.count, D), dtype=torch.float64, pin_memory=True)
         host_x.copy_(x64)
         host_f = torch.empty(args.n, dtype=torch.float64, pin_memory=True)
@@ -526,10 +622,21 @@ def run_ours(args):
                             "H2D, evaluations queued with their NCCL all-gathers overlapped, D2H per function")}
         del host_x, host_f, host_res, res
 
+    if args.config != 5:
+        e2e = e2e_numpy
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sample = x64[: args.cpu_rows * (os.cpu_count() or 1)].cpu().numpy()   # rows 0.. of X
-        cpu = cpu_reference(D, fns, precs, args.cpu_rows, x_rows=sample)
+        # all cores over min(N, --cpu-rows) rows, and one pinned core
+        procs = os.cpu_count() or 1
+        total = min(args.n, args.cpu_rows)
+        per_proc = max(1, -(-total // procs))
+        sample = x64[: per_proc * procs].cpu().numpy()                  # rows 0.. of X
+        cpu = cpu_reference(D, fns, precs, per_proc, x_rows=sample, pin=True)
+        one = cpu_reference(D, fns, precs, min(args.cpu_rows_1core, args.n), x_rows=sample,
+                            procs=1, pin=True)
+        cpu["single_core"] = {"value": one["value"], "unit": UNIT, "cores": 1,
+                              "sample": one["sample"], "pinned": "core 0"}
 
     if args.breakdown and rank == 0:
         Path(args.breakdown).write_text(json.dumps({"rows": rows, "n_local": shard.count,
@@ -542,11 +649,15 @@ def run_ours(args):
             "dtype": "f64+f32" if len(precs) == 2 else ("f64" if precs[0] == "double" else "f32"),
             "data": ("synthetic X = numpy Philox(SeedSequence((0, D, N, 1001))).uniform(-100, 100), "
                      "drawn on the device bit-identically (population.py)"),
-            "config": {"workload": f"suite-sweep D={D} N={args.n} ({len(fns)} fns x {len(precs)} precisions)",
+            "config": {"workload": (f"config {args.config}: {CONFIGS[args.config]['name']}"
+                                    if args.config != 5 else
+                                    f"suite-sweep D={D} N={args.n} ({len(fns)} fns x {len(precs)} precisions)"),
+                       "baseline_config": args.config,
                        "dim": D, "n": args.n, "fns": len(fns), "precisions": precs,
-                       "parallelism": f"rows/{world}", "l2": "inputs larger than L2 (8 GB fp64 + 4 GB fp32)",
+                       "parallelism": f"rows/{world}", "l2": l2_note,
                        "seed": 0},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "e2e_numpy": e2e_numpy if args.config == 5 else None, "latency": latency,
             "clocks": clk,
             "per_precision_evals_per_s": {
                 p: len(fns) * args.n / sum(r["seconds"] for r in rows if r["precision"] == p)

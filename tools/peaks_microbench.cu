@@ -29,6 +29,10 @@ __global__ void k_ffma(float* out, int iters, float a, float b) {
   float s = 0; for (int i = 0; i < ILP; ++i) s += acc[i];
   if (s == 12345.678f) out[0] = s;
 }
+// The exact-order rotate's instruction pair: a rounded product and a rounded
+// add, both operands live (the product depends on the accumulator, so no
+// part of the chain is loop-invariant: r01's version multiplied two
+// invariants, ptxas hoisted the FMULs and the loop timed FADD alone).
 template<int ILP>
 __global__ void k_fmuladd(float* out, int iters, float a, float b) {
   float acc[ILP];
@@ -36,10 +40,23 @@ __global__ void k_fmuladd(float* out, int iters, float a, float b) {
   for (int i = 0; i < ILP; ++i) acc[i] = threadIdx.x * 1e-3f + i;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < ILP; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(b, a + i));
+    for (int i = 0; i < ILP; ++i) acc[i] = __fadd_rn(__fmul_rn(acc[i], a), b);
   }
   float s = 0; for (int i = 0; i < ILP; ++i) s += acc[i];
   if (s == 12345.678f) out[0] = s;
+}
+// float64 DMUL + DADD pair (the exact-order float64 re-evaluation)
+template<int ILP>
+__global__ void k_dmuladd(double* out, int iters, double a, double b) {
+  double acc[ILP];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) acc[i] = __dadd_rn(__dmul_rn(acc[i], a), b);
+  }
+  double s = 0; for (int i = 0; i < ILP; ++i) s += acc[i];
+  if (s == 12345.678) out[0] = s;
 }
 // packed FP32 (sm_100 FFMA2 / FADD2), the exact-order rotate's instruction
 // pair: product as fma(a, b, -0) with an opaque -0, then a separate add
@@ -139,6 +156,8 @@ int main() {
   printf(", \"ffma_tflops\": %.2f", nthr * iters * 8 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&]{ k_fmuladd<8><<<blocks, threads>>>((float*)dout, iters, 1.0000001f, 1e-9f); });
   printf(", \"fmul_fadd_tflops\": %.2f", nthr * iters * 8 * 2 / (ms * 1e-3) / 1e12);
+  ms = timeit([&]{ k_dmuladd<8><<<blocks, threads>>>(dout, iters, 1.0000001, 1e-9); });
+  printf(", \"dmul_dadd_tflops\": %.2f", nthr * iters * 8 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&]{ k_ffma2<8><<<blocks, threads>>>((float*)dout, iters, 1.0000001f, 1e-9f); });
   printf(", \"ffma2_tflops\": %.2f", nthr * iters * 8 * 4 / (ms * 1e-3) / 1e12);
   ms = timeit([&]{ k_fmul2_fadd2<8><<<blocks, threads>>>((float*)dout, iters, 1.0000001f, -0.0f); });
