@@ -139,10 +139,18 @@ rb_status rb_h_func_evaluate (rb_engine* e, int32_t fn_id, const double* x, int6
 rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n,
                               float* f);
 
-/* ---- stream-ordered calls with a deferred status ------------------------ */
-/* precision: RB_DOUBLE (x, f are double*) or RB_SINGLE (float*). */
+/* precision: RB_DOUBLE (double) or RB_SINGLE (float). */
 #define RB_DOUBLE 0
 #define RB_SINGLE 1
+/* Host float64 rows evaluated in `precision`: RB_SINGLE rounds each x to
+ * float32 first, as the reference's Engine.evaluate(..., "single") casts its
+ * float64 batch (engine.py:201), inside the transfer pipeline (no separate
+ * host cast pass); f is double* or float*.  The host wrappers pipeline rows
+ * through pinned chunks: host staging, H2D, evaluation and D2H overlap. */
+rb_status rb_h_func_evaluate_x64(rb_engine* e, int32_t fn_id, int32_t precision, const double* x,
+                                 int64_t n, void* f);
+
+/* ---- stream-ordered calls with a deferred status ------------------------ */
 /* Enqueue the evaluation on `stream` and return at once: argument errors
  * (the reference's validation order) come back now; the input's finiteness
  * (NonFiniteInput) is read later with rb_ticket_status, after the caller has

@@ -9,9 +9,11 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <map>
+#include <thread>
 
 #include "rb_fnspec.cuh"
 
@@ -195,11 +197,14 @@ struct rb_engine {
   int* h_flags = nullptr;                    // ring of per-call non-finite flags, mapped
   int* d_flags = nullptr;                    // pinned host memory (device alias of h_flags)
   std::atomic<uint32_t> next_flag{0};
-  std::mutex host_mu;                        // host-pointer API staging buffers
-  void* stage_x = nullptr;
-  void* stage_f = nullptr;
-  void* pin_x = nullptr;                     // pinned staging of small host batches (x, then f)
-  size_t stage_bytes_x = 0, stage_bytes_f = 0;
+  std::mutex host_mu;                        // host-pointer API pipeline (evaluate_host_locked)
+  void* pin_x[2] = {nullptr, nullptr};       // pinned row chunks
+  void* pin_f[2] = {nullptr, nullptr};       // pinned values of a chunk
+  void* dev_x[2] = {nullptr, nullptr};
+  void* dev_f[2] = {nullptr, nullptr};
+  int64_t chunk_rows = 0;                    // capacity of each buffer, in rows
+  cudaStream_t copy_stream = nullptr;        // H2D of row chunks
+  cudaEvent_t x_ready[2] = {nullptr, nullptr}, f_ready[2] = {nullptr, nullptr};
   cudaStream_t host_stream = nullptr;
 };
 
@@ -227,9 +232,15 @@ void release(rb_engine* e) {
   cudaFree(e->d_index);
   cudaFree(e->d_v64);
   cudaFree(e->d_v32);
-  cudaFree(e->stage_x);
-  cudaFree(e->stage_f);
-  if (e->pin_x) cudaFreeHost(e->pin_x);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(e->dev_x[b]);
+    cudaFree(e->dev_f[b]);
+    if (e->pin_x[b]) cudaFreeHost(e->pin_x[b]);
+    if (e->pin_f[b]) cudaFreeHost(e->pin_f[b]);
+    if (e->x_ready[b]) cudaEventDestroy(e->x_ready[b]);
+    if (e->f_ready[b]) cudaEventDestroy(e->f_ready[b]);
+  }
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->h_flags) cudaFreeHost(e->h_flags);
   if (e->host_stream) cudaStreamDestroy(e->host_stream);
   cudaSetDevice(prev);
@@ -364,63 +375,127 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
   return s;
 }
 
-// Host-pointer call (device current, host_mu held): one H2D, the launch,
-// one D2H and a single synchronisation.  Batches up to kPinnedStage bytes
-// go through pinned staging buffers (fast async copies, f written only on
-// success); larger ones copy from / to the caller's pageable memory.
-constexpr size_t kPinnedStage = size_t(8) << 20;
+// Host-pointer call (device current, host_mu held), pipelined in row chunks
+// of ~kChunkBytes: while the GPU copies chunk c in (copy stream), evaluates
+// it and copies its values out (engine stream), host threads stage chunk
+// c+1 into the other pinned buffer -- a copy, or for float64 rows
+// evaluated in float32 the rounding engine.py:201 does (astype = round to
+// nearest) -- and the values of chunk c-1 leave their pinned buffer for the
+// caller's f.  A batch of one chunk is one H2D, one launch, one D2H.  On an
+// error the contents of f are unspecified (the reference returns nothing).
+constexpr size_t kChunkBytes = size_t(32) << 20;
 
-template <class T>
-rb_status evaluate_host_locked(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
-  const size_t bx = sizeof(T) * (size_t)n * e->dim, bf = sizeof(T) * (size_t)n;
-  if (bx > e->stage_bytes_x) {
-    cudaFree(e->stage_x);
-    e->stage_x = nullptr;
-    RB_CUDA(cudaMalloc(&e->stage_x, bx));
-    e->stage_bytes_x = bx;
+template <class F>
+void parallel_rows(int64_t n, int64_t bytes, F&& fn) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = bytes >= (int64_t(1) << 21) ? std::min(8, hw) : 1;
+  if (nt <= 1 || n < 2 * nt) {
+    fn(int64_t(0), n);
+    return;
   }
-  if (bf > e->stage_bytes_f) {
-    cudaFree(e->stage_f);
-    e->stage_f = nullptr;
-    RB_CUDA(cudaMalloc(&e->stage_f, bf));
-    e->stage_bytes_f = bf;
+  std::vector<std::thread> ts;
+  const int64_t per = (n + nt - 1) / nt;
+  for (int t = 1; t < nt; ++t) {
+    const int64_t lo = t * per, hi = std::min(n, lo + per);
+    if (lo < hi) ts.emplace_back([&fn, lo, hi] { fn(lo, hi); });
   }
-  const size_t fo = (bx + 255) & ~size_t(255);       // f's offset in the pinned buffer
-  const bool pinned = fo + bf <= kPinnedStage;
-  if (pinned && !e->pin_x) RB_CUDA(cudaMallocHost(&e->pin_x, kPinnedStage));
-  const void* src = x;
-  void* dst = f;
-  if (pinned) {
-    std::memcpy(e->pin_x, x, bx);
-    src = e->pin_x;
-    dst = static_cast<unsigned char*>(e->pin_x) + fo;
+  fn(int64_t(0), std::min(n, per));
+  for (auto& th : ts) th.join();
+}
+
+rb_status ensure_pipeline(rb_engine* e) {
+  if (e->chunk_rows > 0) return RB_OK;
+  const int64_t rows = std::max<int64_t>(1, (int64_t)(kChunkBytes / (sizeof(double) * e->dim)));
+  for (int b = 0; b < 2; ++b) {
+    RB_CUDA(cudaMallocHost(&e->pin_x[b], sizeof(double) * rows * e->dim));
+    RB_CUDA(cudaMallocHost(&e->pin_f[b], sizeof(double) * rows));
+    RB_CUDA(cudaMalloc(&e->dev_x[b], sizeof(double) * rows * e->dim));
+    RB_CUDA(cudaMalloc(&e->dev_f[b], sizeof(double) * rows));
+    RB_CUDA(cudaEventCreateWithFlags(&e->x_ready[b], cudaEventDisableTiming));
+    RB_CUDA(cudaEventCreateWithFlags(&e->f_ready[b], cudaEventDisableTiming));
   }
-  RB_CUDA(cudaMemcpyAsync(e->stage_x, src, bx, cudaMemcpyHostToDevice, e->host_stream));
-  volatile int* flag = nullptr;
-  rb_status s = launch_eval<T>(e, fn_id, static_cast<const T*>(e->stage_x), n,
-                               static_cast<T*>(e->stage_f), e->host_stream, &flag, true);
-  if (s != RB_OK) {
-    cudaStreamSynchronize(e->host_stream);
-    return s;
-  }
-  RB_CUDA(cudaMemcpyAsync(dst, e->stage_f, bf, cudaMemcpyDeviceToHost, e->host_stream));
-  RB_CUDA(cudaStreamSynchronize(e->host_stream));
-  if (flag[0]) return non_finite();
-  if (pinned) std::memcpy(f, dst, bf);
+  RB_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+  e->chunk_rows = rows;
   return RB_OK;
 }
 
-template <class T>
-rb_status evaluate_host(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
+// TI: the caller's element type; T: the evaluation precision
+template <class TI, class T>
+rb_status evaluate_host_locked(rb_engine* e, int32_t fn_id, const TI* x, int64_t n, T* f) {
+  {
+    const rb_status st = ensure_pipeline(e);
+    if (st != RB_OK) return st;
+  }
+  const int dim = e->dim;
+  const int64_t cap = e->chunk_rows;
+  const int64_t nchunks = (n + cap - 1) / cap;
+  std::vector<volatile int*> flags;
+  flags.reserve(nchunks);
+  auto drain = [&](int64_t c) -> rb_status {   // chunk c's values into the caller's f
+    const int b = (int)(c & 1);
+    RB_CUDA(cudaEventSynchronize(e->f_ready[b]));
+    const int64_t r0 = c * cap, rows = std::min(cap, n - r0);
+    std::memcpy(f + r0, e->pin_f[b], sizeof(T) * rows);
+    return RB_OK;
+  };
+  rb_status st = RB_OK;
+  for (int64_t c = 0; c < nchunks && st == RB_OK; ++c) {
+    const int b = (int)(c & 1);
+    if (c >= 2) {                              // buffers b free: chunk c-2 is done
+      st = drain(c - 2);
+      if (st != RB_OK) break;
+    }
+    const int64_t r0 = c * cap, rows = std::min(cap, n - r0);
+    T* px = static_cast<T*>(e->pin_x[b]);
+    const TI* src = x + r0 * dim;
+    parallel_rows(rows, (int64_t)sizeof(T) * rows * dim, [&](int64_t lo, int64_t hi) {
+      if constexpr (std::is_same<TI, T>::value) {
+        std::memcpy(px + lo * dim, src + lo * dim, sizeof(T) * (hi - lo) * dim);
+      } else {
+        for (int64_t i = lo * dim; i < hi * dim; ++i) px[i] = static_cast<T>(src[i]);
+      }
+    });
+    if (cudaMemcpyAsync(e->dev_x[b], px, sizeof(T) * rows * dim, cudaMemcpyHostToDevice,
+                        e->copy_stream) != cudaSuccess ||
+        cudaEventRecord(e->x_ready[b], e->copy_stream) != cudaSuccess ||
+        cudaStreamWaitEvent(e->host_stream, e->x_ready[b], 0) != cudaSuccess) {
+      st = fail(RB_E_CUDA, "host pipeline: H2D failed");
+      break;
+    }
+    volatile int* flag = nullptr;
+    st = launch_eval<T>(e, fn_id, static_cast<const T*>(e->dev_x[b]), rows,
+                        static_cast<T*>(e->dev_f[b]), e->host_stream, &flag, true);
+    if (st != RB_OK) break;
+    flags.push_back(flag);
+    if (cudaMemcpyAsync(e->pin_f[b], e->dev_f[b], sizeof(T) * rows, cudaMemcpyDeviceToHost,
+                        e->host_stream) != cudaSuccess ||
+        cudaEventRecord(e->f_ready[b], e->host_stream) != cudaSuccess)
+      st = fail(RB_E_CUDA, "host pipeline: D2H failed");
+  }
+  if (st == RB_OK)
+    for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks && st == RB_OK; ++c) st = drain(c);
+  cudaStreamSynchronize(e->host_stream);
+  cudaStreamSynchronize(e->copy_stream);
+  if (st != RB_OK) return st;
+  for (volatile int* fl : flags)
+    if (fl[0]) return non_finite();
+  return RB_OK;
+}
+
+template <class TI, class T>
+rb_status evaluate_host(rb_engine* e, int32_t fn_id, const TI* x, int64_t n, T* f) {
   if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
   if (n < 1 || n > e->max_concurrency || !x || !f || fn_id < 0 ||
       fn_id >= (int32_t)e->fns.size() || e->fns[fn_id].category == RB_DISABLED)
-    return evaluate_device<T>(e, fn_id, x, n, f, nullptr);   // reports the error
+    return evaluate_device<T>(e, fn_id, reinterpret_cast<const T*>(x), n, f, nullptr);  // the error
+  const int pi = sizeof(T) == 8 ? 0 : 1;
+  if (!e->why[pi][fn_id].empty())
+    return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fn_id) + ": " + e->why[pi][fn_id]);
   std::lock_guard<std::mutex> lock(e->host_mu);
   int prev = 0;
   RB_CUDA(cudaGetDevice(&prev));
   RB_CUDA(cudaSetDevice(e->device));
-  const rb_status s = evaluate_host_locked<T>(e, fn_id, x, n, f);
+  const rb_status s = evaluate_host_locked<TI, T>(e, fn_id, x, n, f);
   cudaSetDevice(prev);
   return s;
 }
@@ -866,11 +941,18 @@ rb_status rb_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t
 }
 
 rb_status rb_h_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64_t n, double* f) {
-  return evaluate_host<double>(e, fn_id, x, n, f);
+  return evaluate_host<double, double>(e, fn_id, x, n, f);
 }
 
 rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f) {
-  return evaluate_host<float>(e, fn_id, x, n, f);
+  return evaluate_host<float, float>(e, fn_id, x, n, f);
+}
+
+rb_status rb_h_func_evaluate_x64(rb_engine* e, int32_t fn_id, int32_t precision, const double* x,
+                                 int64_t n, void* f) {
+  if (precision == RB_DOUBLE) return evaluate_host<double, double>(e, fn_id, x, n, static_cast<double*>(f));
+  if (precision == RB_SINGLE) return evaluate_host<double, float>(e, fn_id, x, n, static_cast<float*>(f));
+  return fail(RB_E_INVALID_ARGUMENT, "precision must be RB_DOUBLE or RB_SINGLE");
 }
 
 rb_status rb_func_evaluate_async(rb_engine* e, int32_t fn_id, int32_t precision, const void* x,

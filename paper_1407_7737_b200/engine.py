@@ -234,9 +234,18 @@ class Engine:
     # -- paths
     def _evaluate_host(self, fn_id, data, precision):
         dt = _DTYPES[precision]
+        lib = _lib.load()
+        if dt is np.float32 and data.dtype == np.float64:
+            # engine.py:201's float32 cast, done per row chunk inside the
+            # native transfer pipeline (rb_h_func_evaluate_x64)
+            pts = np.ascontiguousarray(data)
+            out = np.empty(pts.shape[0], dtype=dt)
+            _lib.check(lib.rb_h_func_evaluate_x64(self._handle, fn_id, _lib.RB_SINGLE, _lib.ptr(pts),
+                                                  pts.shape[0], _lib.ptr(out)))
+            return out
         pts = np.ascontiguousarray(data, dtype=dt)          # engine.py:201
         out = np.empty(pts.shape[0], dtype=dt)
-        call = _lib.load().rb_h_func_evaluate if dt is np.float64 else _lib.load().rb_h_func_evaluatef
+        call = lib.rb_h_func_evaluate if dt is np.float64 else lib.rb_h_func_evaluatef
         _lib.check(call(self._handle, fn_id, _lib.ptr(pts), pts.shape[0], _lib.ptr(out)))
         return out
 

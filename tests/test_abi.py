@@ -15,7 +15,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "robench_b200.h"
 
 def declared():
     text = HEADER.read_text()
-    decl = r"^(?:rb_status|int32_t|int64_t|void|const char\*)\s+(rb_[a-z_]+)\s*\("
+    decl = r"^(?:rb_status|int32_t|int64_t|void|const char\*)\s+(rb_[a-z0-9_]+)\s*\("
     return sorted(set(re.findall(decl, text, flags=re.M)))
 
 

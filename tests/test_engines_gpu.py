@@ -92,3 +92,34 @@ def test_near_optimum_rows_take_the_exact_order_pass(dim):
             assert eng.evaluate(fn, x[i:i + 1]).values[0] == host[i], (fn, i)
         assert _lib.launch_count() - n0 >= 3          # main kernel + fixup passes ran
     eng.dispose()
+
+
+def test_host_pipeline_chunks_match_the_device_path():
+    # rb_h_func_evaluate[f] / _x64 pipeline rows in ~32 MB chunks (41 943
+    # rows at D=100): a 3-chunk batch equals the device-tensor evaluation bit
+    # for bit in both precisions (float32 from float64 rows = the host cast
+    # of engine.py:201); a NaN in the last chunk raises; a HappyCat optimum in
+    # the second chunk takes the fixup pass
+    import torch
+    from paper_1407_7737_b200 import instances
+    dim, n = 100, 100_003
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=n, seed=0))
+    x = population(dim, n, seed=9)
+    x[50_000] = instances.build(20, dim, 0).shift
+    xt = torch.from_numpy(x).cuda()
+    for fn in (0, 20, 33):
+        for prec in ("double", "single"):
+            host = eng.evaluate(fn, x, precision=prec).values
+            dev = eng.evaluate(fn, xt, precision=prec).values.cpu().numpy()
+            assert host.dtype == (np.float64 if prec == "double" else np.float32)
+            assert np.array_equal(host, dev), (fn, prec)
+    x32 = x.astype(np.float32)
+    assert np.array_equal(eng.evaluate(8, x32, precision="single").values,
+                          eng.evaluate(8, x, precision="single").values)
+    assert eng.evaluate(20, x).values[50_000] == 100.0
+    bad = x.copy()
+    bad[n - 2, 7] = np.nan
+    for prec in ("double", "single"):
+        with pytest.raises(rb.NonFiniteInput):
+            eng.evaluate(0, bad, precision=prec)
+    eng.dispose()
