@@ -1316,6 +1316,11 @@ template <class T>
 __global__ void __launch_bounds__(NT, 1) fixup_kernel(const Args<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);
+  // queued behind its kernel by callers that do not read the flags first
+  // (rb_func_evaluate_async): nothing marked -> done, before any plan work
+  if (threadIdx.x == 0) s.P->marked = (uint32_t)reinterpret_cast<volatile int*>(a.flag)[1];
+  __syncthreads();
+  if (!s.P->marked) return;
   load_plan(a, s);
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
