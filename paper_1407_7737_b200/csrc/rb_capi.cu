@@ -545,7 +545,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
         for (int g = sg.group0; g < sg.group0 + sg.n_groups; ++g) {
           max_q += rb::round8(pk->groups[g].m);
           q4 += (pk->groups[g].m + 3) & ~3;
-          units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);
+          units += (rb::TP / 16) * ((pk->groups[g].m + 7) / 8);   // (MT2 kernels: half)
           deep = deep || pk->groups[g].leaf == -2;
         }
       }

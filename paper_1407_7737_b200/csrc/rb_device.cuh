@@ -62,6 +62,14 @@ constexpr int MAX_MEMBERS = 5;
 constexpr int MAX_SEGMENTS = 16;
 constexpr int MAX_GROUPS = 16;
 constexpr int MAX_UNITS = 512;  // fp64 DMMA units (m-tile x n-tile of a group) per function
+// MT2 (float64 DMMA rotate): one unit covers both 16-point m-tiles of the
+// tile, so each B fragment load feeds twice the DMMAs (half the B traffic
+// from L1 / L2).  Measured: basic functions +0-4 %, hybrids +5-8 %;
+// compositions -10-20 % (the extra accumulators spill at their register
+// budget), which keep one m-tile per unit.
+static_assert(TP == 32, "MT2 units cover the tile's two m-tiles");
+template <int KID>
+__host__ __device__ constexpr bool mt2_kernel() { return KID >= 0 && KID < 100 + 29; }   // basic + hybrids 23-28
 constexpr int NTC = 2;          // DMMA n-tiles (8 rows) sharing one A fragment per k-step
                                 // (3 measured: +1-3% basic, -10-18% compositions: spills)
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
@@ -226,7 +234,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // memory and build the per-column gather tables (padded to 8 columns with
 // column 0 and optimum 0: finite values times zero B entries) and the
 // per-row scatter table.
-template <class T>
+template <class T, bool MT2 = false>
 __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
   PlanHead& P = *s.P;
   if (threadIdx.x == 0) {
@@ -271,7 +279,7 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
       const int g0 = P.seg[si].group0 - P.grp_base;
       for (int g = g0; g < g0 + P.seg[si].n_groups; ++g) P.grp_seg[g] = (int8_t)si;
       for (int g = g0; g < g0 + P.seg[si].n_groups; ++g)
-        for (int mt = 0; mt < TP / 16; ++mt)
+        for (int mt = 0; mt < TP / 16; mt += (MT2 ? 2 : 1))
           for (int nt = 0; nt < (P.grp[g].m + 7) >> 3 && nu < MAX_UNITS; ++nt)
             P.unit[nu++] = (uint32_t)g | ((uint32_t)mt << 8) | ((uint32_t)nt << 16);
     }
@@ -437,7 +445,71 @@ __device__ __forceinline__ void dmma_run(const double* X0, const double* X1, con
   }
 }
 
-template <int NW, bool CHECK>
+// epilogue of one m-tile: z = acc - cz, scattered to the rows' z positions;
+// rows come in pairs (2 tig, 2 tig + 1), so the tables are read as pairs
+template <bool CHECK>
+__device__ __forceinline__ void dmma_epilogue(const Args<double>& a, const Smem<double>& s,
+                                              const rb_group& G, const double (&acc)[2][4], int mt,
+                                              int nt0, int run, int gid, int tig, uint32_t& nf) {
+  const PlanHead& P = *s.P;
+  const int g = (int)(&G - P.grp);
+  const int m = G.m;
+  const int* prow = s.prow + P.gq0[g];
+  const double* cz = s.cz + P.gq0[g];
+  const int p0 = mt * 16 + gid;
+  double* Z0 = s.ZS + p0 * a.ldz;
+  double* Z1 = Z0 + 8 * a.ldz;
+  uint32_t e0 = 0u, e1 = 0u;                  // max exponent field per point
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int rr = (nt0 + c) * 8 + 2 * tig;
+    if (c < run && rr < m) {
+      const int2 pr = *reinterpret_cast<const int2*>(prow + rr);
+      const double2 cc = *reinterpret_cast<const double2*>(cz + rr);
+      const double z00 = acc[c][0] - cc.x, z10 = acc[c][2] - cc.x;
+      Z0[pr.x] = z00;
+      Z1[pr.x] = z10;
+      double z01 = 0.0, z11 = 0.0;
+      if (rr + 1 < m) {
+        z01 = acc[c][1] - cc.y;
+        z11 = acc[c][3] - cc.y;
+        Z0[pr.y] = z01;
+        Z1[pr.y] = z11;
+      }
+      if (CHECK) {
+        e0 = max(e0, max((uint32_t)__double2hiint(z00), (uint32_t)__double2hiint(z01)) & 0x7ff00000u);
+        e1 = max(e1, max((uint32_t)__double2hiint(z10), (uint32_t)__double2hiint(z11)) & 0x7ff00000u);
+      }
+    }
+  }
+  if (CHECK && e0 == 0x7ff00000u) nf |= 1u << p0;      // NaN or infinity (kernels.py:45-49)
+  if (CHECK && e1 == 0x7ff00000u) nf |= 1u << (p0 + 8);
+}
+
+// Both m-tiles of the tile (MT2): each B fragment load feeds 2 x R
+// DMMAs (the two 16-point m-tiles), halving the B traffic from L1 / L2.
+template <int R>
+__device__ __forceinline__ void dmma_run_mt2(const double* X0, const double* X1, const double* X2,
+                                             const double* X3, const int* qs, const double* qo,
+                                             const double* F, int nks, double (&acc)[2][2][4]) {
+#pragma unroll 2
+  for (int ks = 0; ks < nks; ++ks) {
+    const int col = qs[ks * 4];
+    const double o = qo[ks * 4];
+    const double b0 = __ldg(F + ks * 32);
+    const double a0 = X0[col] - o, a1 = X1[col] - o;
+    const double a2 = X2[col] - o, a3 = X3[col] - o;
+    dmma_16x8x4(acc[0][0], a0, a1, b0);
+    dmma_16x8x4(acc[1][0], a2, a3, b0);
+    if constexpr (R == 2) {
+      const double b1 = __ldg(F + (nks + ks) * 32);
+      dmma_16x8x4(acc[0][1], a0, a1, b1);
+      dmma_16x8x4(acc[1][1], a2, a3, b1);
+    }
+  }
+}
+
+template <int NW, bool CHECK, bool MT2>
 __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int s_first,
                                       int s_end, int warp) {
   const PlanHead& P = *s.P;
@@ -458,52 +530,35 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
     const double* qo = s.qo + P.gq0[g] + tig;
     const double* X0 = s.XS + (mt * 16 + gid) * a.dim;
     const double* X1 = X0 + 8 * a.dim;
+    if constexpr (MT2) {
+    double acc2[2][2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc2[i][j][k] = 0.0;
+    if (run == 2) dmma_run_mt2<2>(X0, X1, X0 + 16 * a.dim, X1 + 16 * a.dim, qs, qo, F, nks, acc2);
+    else dmma_run_mt2<1>(X0, X1, X0 + 16 * a.dim, X1 + 16 * a.dim, qs, qo, F, nks, acc2);
+#pragma unroll
+    for (int mh = 0; mh < 2; ++mh) dmma_epilogue<CHECK>(a, s, G, acc2[mh], mt + mh, nt0, run, gid, tig, nf);
+    } else {
     double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
     // the run length is warp-uniform: unpredicated mma.sync in both loops
     if (run == 2) dmma_run<2>(X0, X1, qs, qo, F, nks, acc);
     else dmma_run<1>(X0, X1, qs, qo, F, nks, acc);
-    // epilogue: z = acc - cz, scattered to the rows' z positions; rows come
-    // in pairs (2 tig, 2 tig + 1), so the tables are read as pairs
-    const int* prow = s.prow + P.gq0[g];
-    const double* cz = s.cz + P.gq0[g];
-    const int p0 = mt * 16 + gid;
-    double* Z0 = s.ZS + p0 * a.ldz;
-    double* Z1 = Z0 + 8 * a.ldz;
-    uint32_t e0 = 0u, e1 = 0u;                  // max exponent field per point
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int rr = (nt0 + c) * 8 + 2 * tig;
-      if (c < run && rr < m) {
-        const int2 pr = *reinterpret_cast<const int2*>(prow + rr);
-        const double2 cc = *reinterpret_cast<const double2*>(cz + rr);
-        const double z00 = acc[c][0] - cc.x, z10 = acc[c][2] - cc.x;
-        Z0[pr.x] = z00;
-        Z1[pr.x] = z10;
-        double z01 = 0.0, z11 = 0.0;
-        if (rr + 1 < m) {
-          z01 = acc[c][1] - cc.y;
-          z11 = acc[c][3] - cc.y;
-          Z0[pr.y] = z01;
-          Z1[pr.y] = z11;
-        }
-        if (CHECK) {
-          e0 = max(e0, max((uint32_t)__double2hiint(z00), (uint32_t)__double2hiint(z01)) & 0x7ff00000u);
-          e1 = max(e1, max((uint32_t)__double2hiint(z10), (uint32_t)__double2hiint(z11)) & 0x7ff00000u);
-        }
-      }
+    dmma_epilogue<CHECK>(a, s, G, acc, mt, nt0, run, gid, tig, nf);
     }
-    if (CHECK && e0 == 0x7ff00000u) nf |= 1u << p0;      // NaN or infinity (kernels.py:45-49)
-    if (CHECK && e1 == 0x7ff00000u) nf |= 1u << (p0 + 8);
     u += run;
   }
   return nf;
 }
 
 // z of plan segments [s_first, s_end) (the chunks of one member, side by side)
-template <bool CHECK>
+template <bool CHECK, bool MT2 = false>
 __device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, int s_first,
                                   int s_end) {
-  return rotate_f64<NWARPS, CHECK>(a, s, s_first, s_end, threadIdx.x >> 5);
+  return rotate_f64<NWARPS, CHECK, MT2>(a, s, s_first, s_end, threadIdx.x >> 5);
 }
 
 // ------------------------------------------------------------ rotate fp32
@@ -647,7 +702,7 @@ __device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int 
 }
 
 // the V tile is in place (gather_v + barrier)
-template <bool CHECK>
+template <bool CHECK, bool MT2 = false>
 __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, int s_first,
                                   int s_end) {
   const PlanHead& P = *s.P;
@@ -974,7 +1029,7 @@ __device__ __forceinline__ void issue_next_x(const Args<T>& a, const Smem<T>& s,
 // where z lives (row stride ldz).
 // EXACT (float64, fixup_kernel): members with an exact-order path
 // (P.exact_mem) rotate in NumPy's order instead of by DMMA.
-template <class T, bool EXACT = false>
+template <class T, bool EXACT = false, bool MT2 = false>
 __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
                                  TileCtx& t) {
   const PlanHead& P = *s.P;
@@ -1013,7 +1068,7 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
       else
         nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
     } else {
-      nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
+      nf = t.check_z ? rotate<true, MT2>(a, s, s_first, s_end) : rotate<false, MT2>(a, s, s_first, s_end);
     }
   }
   if (nf & t.live) raise_flag(a);
@@ -1034,7 +1089,7 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
   RB_PHASE_MARK(c0);
-  const T* zb = stage_member<T, KID == FIXUP>(a, s, mem, t);
+  const T* zb = stage_member<T, KID == FIXUP, mt2_kernel<KID>()>(a, s, mem, t);
   if (last) issue_next_x(a, s, t);
   RB_PHASE_MARK(c1);
   // compile-time: can this kernel meet a float64 exact64 member at all?
@@ -1200,7 +1255,7 @@ __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     evaluate_kernel(const Args<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);
-  load_plan(a, s);
+  load_plan<T, mt2_kernel<KID>()>(a, s);
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;

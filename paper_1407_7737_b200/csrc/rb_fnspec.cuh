@@ -124,7 +124,7 @@ __device__ T spec_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, bool val
     }
     const rb_member& mem = P.mem[mi];
     RB_PHASE_MARK(c0);
-    const T* zb = stage_member(a, s, mem, t);
+    const T* zb = stage_member<T, false, mt2_kernel<SPEC_BASE + FID>()>(a, s, mem, t);
     if (j1 == L.n) issue_next_x(a, s, t);
     RB_PHASE_MARK(c1);
     constexpr bool kMark = sizeof(T) == 8 && has_exact64(FID);
