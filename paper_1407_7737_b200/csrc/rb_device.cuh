@@ -35,6 +35,9 @@
 #define RB_F32_UNROLL 2           // column-loop unroll of the float32 rotate slots
 #endif
 constexpr int kF32Unroll = RB_F32_UNROLL;
+#ifndef RB_F32_FAST_WEIGHTS
+#define RB_F32_FAST_WEIGHTS 1
+#endif
 #ifndef RB_F32_ROWS
 #define RB_F32_ROWS 4             // rows per pass of the float32 rotate tile (4 or 2)
 #endif
@@ -1182,9 +1185,23 @@ __device__ __forceinline__ void composition_weights(const Args<T>& a, const Plan
 #pragma unroll
   for (int k = 1; k < MAX_MEMBERS; ++k)
     if (l8 == k && k < nm) { dk = d2[k]; sgk = (T)P.mem[k].sigma; }
-  // d2 ** -0.5: float64 to tolerance via rsqrt; float32 NumPy's SVML powf
+  // d2 ** -0.5 and the Gaussian factor, to tolerance in both precisions: the
+  // weights enter the value linearly (omega * (lambda G + bias)), so an ulp
+  // in w is an ulp-level relative change of the value (float32: rsqrtf and
+  // expf on the FP32 / XU pipes, not NumPy's SVML powf and a double exp)
+#if RB_F32_FAST_WEIGHTS
+  T ih, wk;
+  if constexpr (sizeof(T) == 8) {
+    ih = (T)::rsqrt((double)dk);
+    wk = ih * M<T>::exp(-dk / (C<T>(2.0 * dim) * (sgk * sgk)));
+  } else {
+    ih = ::rsqrtf((float)dk);
+    wk = ih * ::expf(-dk / (C<T>(2.0 * dim) * (sgk * sgk)));
+  }
+#else
   const T ih = sizeof(T) == 8 ? (T)::rsqrt((double)dk) : apow<T>(dk, C<T>(-0.5));
   const T wk = ih * M<T>::exp(-dk / (C<T>(2.0 * dim) * (sgk * sgk)));
+#endif
   T w[MAX_MEMBERS];
 #pragma unroll
   for (int k = 0; k < MAX_MEMBERS; ++k) w[k] = __shfl_sync(RB_FULL, wk, k, 8);

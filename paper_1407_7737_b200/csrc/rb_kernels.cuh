@@ -128,6 +128,10 @@ template <class T> struct WeierTab { T a[21]; T c[21]; };
 #define RB_WEI_UNROLL 7
 #endif
 constexpr int kWeiUnroll = RB_WEI_UNROLL;   // series terms unrolled per pass (register budget)
+#ifndef RB_WEI_UNROLL_F32
+#define RB_WEI_UNROLL_F32 21          // float: all 21 terms (c_k as constant-bank operands): +3-4 %
+#endif
+constexpr int kWeiUnrollF32 = RB_WEI_UNROLL_F32;
 static __constant__ WeierTab<double> kWei64;
 static __constant__ WeierTab<float> kWei32;
 template <class T> __device__ __forceinline__ const WeierTab<T>& wei_tab();
@@ -161,7 +165,7 @@ template <> __device__ __forceinline__ float weier_coord<float>(float zj, const 
   // sum_k 2^-k cos_k as a Horner chain from k = 20 down (a_k = 0.5^k, so
   // s * 0.5 is exact): no a_k loads in the loop
   float s = 0.0f;
-#pragma unroll kWeiUnroll
+#pragma unroll kWeiUnrollF32
   for (int k = 20; k >= 0; --k) {
     const float x = W.c[k] * w;
     int q;
