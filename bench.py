@@ -26,9 +26,10 @@ Keys beyond the base contract:
                 F = 2*nnz of the rotations applied; P_fp = measured DMMA fp64
                 (fp64) or exact-order FMUL+FADD (fp32) peak on this pool
                 (profiles/r02/peaks.json), HBM from MEASURED_PEAKS.json.
-  cpu_baseline  the reference path (CPU oracle port, per-point NumPy loop as
-                engine.py:205-209) timed on a bounded row sample on all host
-                cores, rank 0, N=1 only.
+  cpu_baseline  the reference's CPU path (the reference package installed in
+                baseline/_ref -- else the bit-identical oracle port -- its
+                per-point NumPy loop, engine.py:205-209) on min(N, 20000) rows
+                on all host cores, plus one pinned core; rank 0, N=1 only.
 """
 
 from __future__ import annotations
@@ -49,6 +50,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "function evals/sec at D=100 FP64/FP32 vs CPU ref; fraction of roofline"
+REF_INSTALL = ROOT / "baseline" / "_ref"       # tools/install_reference.sh
 UNIT = "evals/s"
 PREC = ("double", "single")
 
@@ -229,16 +231,32 @@ def _cpu_worker(job):
             os.sched_setaffinity(0, {core})
         except (AttributeError, OSError):
             pass
-    from oracle.robench_oracle import Oracle
-    orc = Oracle(dim, 0)
-    for fn in fns:                      # build outside the timed loop (initialize)
-        for p in precs:
-            orc.evaluator(fn, p)
+    if (REF_INSTALL / "robench").exists():
+        # the reference itself (tools/install_reference.sh -> baseline/_ref):
+        # robench.initialize + Engine.evaluate, its per-point loop
+        # (engine.py:205-209); initialize (every evaluator) outside the timing
+        sys.path.insert(0, str(REF_INSTALL))
+        import robench
+        eng = robench.initialize(robench.EngineConfig(dim=dim, max_concurrency=max(rows.shape[0], 1),
+                                                      seed=0, threads=1))
+        batch = robench.PointBatch(rows)
+
+        def run(fn, p):
+            eng.evaluate(fn, batch, p)
+    else:
+        from oracle.robench_oracle import Oracle
+        orc = Oracle(dim, 0)
+        for fn in fns:                  # build outside the timed loop (initialize)
+            for p in precs:
+                orc.evaluator(fn, p)
+
+        def run(fn, p):
+            orc.evaluate(fn, rows, p)
     t0 = time.perf_counter()
     n = 0
     for fn in fns:
         for p in precs:
-            orc.evaluate(fn, rows, p)
+            run(fn, p)
             n += rows.shape[0]
     return n, time.perf_counter() - t0
 
@@ -261,10 +279,13 @@ def cpu_reference(dim, fns, precs, rows_per_proc, x_rows=None, procs=None, n_tot
         res = pool.map(_cpu_worker, jobs)
     evals = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
-    return {"value": evals / wall, "unit": UNIT, "cores": procs, "kind": "port",
+    ref = (REF_INSTALL / "robench").exists()
+    return {"value": evals / wall, "unit": UNIT, "cores": procs, "kind": "reference" if ref else "port",
             "sample": (f"{rows_per_proc * procs} rows x {len(fns)} fns x {len(precs)} precisions "
                        f"at D={dim} ({procs} processes x {rows_per_proc} rows, per-point NumPy "
-                       f"loop = engine.py:205-209, oracle/robench_oracle.py)"),
+                       f"loop = engine.py:205-209; "
+                       + ("the reference package itself, baseline/_ref" if ref else
+                          "oracle/robench_oracle.py, the bit-identical port") + ")"),
             "cpu_seconds": sum(r[1] for r in res)}
 
 
@@ -285,6 +306,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * 37 * len(precs) * args.n / value,
+        "ms_per_step_note": ("projected: the full step (every function on all N rows) at the "
+                             "sampled rate; each timed step runs the stated row sample"),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64+f32",
         "data": "synthetic X = numpy Philox(SeedSequence((0, D, N, 1001))).uniform(-100, 100), first rows",
@@ -372,7 +395,7 @@ def run_ours(args):
                                            out=full_bufs[p][k % 2] if full_bufs else None))
                 if record:
                     e1.record(stream)
-                    per.setdefault((fn, p), []).append((e0, e1))
+                    per.setdefault((fn, p), []).append((e0, e1, 1))
         for pd in pend:                  # the comm stream's tail joins the step
             stream.wait_event(pd.done)
         step.calls += len(pend)
@@ -384,8 +407,22 @@ def run_ours(args):
         for pd in pend:
             pd.result()
 
+    # world == 1: a step is ONE native call queueing every (function,
+    # precision) evaluation (Engine.evaluate_many -> rb_func_evaluate_many),
+    # so the device time is not bounded by per-call Python work at small N;
+    # N > 1 GPUs: per-call submits, each with its fitness all-gather
+    calls = [(fn, p) for p in precs for fn in fns]
+    out_bufs = {p: local_bufs[p][0] for p in precs}
+
+    def step_many():
+        k0 = step.calls
+        step.calls += len(calls)
+        return engine.evaluate_many(calls, [xrot[(k0 + i) % n_rot][p] for i, (fn, p) in enumerate(calls)],
+                                    outs=[out_bufs[p] for _, p in calls])
+
+    timed_step = step_many if world == 1 else (lambda: step(False))
     for _ in range(args.warmup):
-        check(step(False))
+        check(timed_step())
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -394,7 +431,7 @@ def run_ours(args):
     launches0 = _lib.launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    pends = [step(True) for _ in range(args.steps)]
+    pends = [timed_step() for _ in range(args.steps)]
     t_end.record(stream)
     torch.cuda.synchronize()
     for pd in pends:
@@ -404,6 +441,21 @@ def run_ours(args):
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     ms = t_start.elapsed_time(t_end)
+    # per-(function, precision) device times (untimed pass): CUDA events
+    # around R back-to-back calls of each, queued in one native call (R > 1
+    # at small N, where a single launch is shorter than the host work per call)
+    reps = 1 if shard.count >= 1_000_000 else 8
+    for fn, p in calls:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0 = step.calls
+        step.calls += reps
+        e0.record(stream)
+        pd = engine.evaluate_many([(fn, p)] * reps, [xrot[(k0 + i) % n_rot][p] for i in range(reps)],
+                                  outs=[out_bufs[p]] * reps)
+        e1.record(stream)
+        per[(fn, p)] = [(e0, e1, reps)]
+        check(pd)
+    torch.cuda.synchronize()
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -423,7 +475,7 @@ def run_ours(args):
             "single": float(mypk.get("fmul_fadd_tflops", 36.6)) * 1e12}
     rows = []
     for (fn, p), evs in per.items():
-        t = sum(a.elapsed_time(b) for a, b in evs) / 1e3 / len(evs)
+        t = sum(a.elapsed_time(b) / r for a, b, r in evs) / 1e3 / len(evs)
         s = 8 if p == "double" else 4
         t_hbm = shard.count * (D + 1) * s / hbm
         t_fp = shard.count * flops[fn] / p_fp[p]
@@ -492,12 +544,13 @@ def run_ours(args):
                               "float32 calls cast X on the host first, as the reference does (engine.py:201)"),
                      "timing": "host wall clock around the blocking calls"}
         if args.config == 1:
-            dev_us = sorted(1e3 * a.elapsed_time(b) for evs in per.values() for a, b in evs)
+            dev_us = sorted(1e3 * a.elapsed_time(b) / r for evs in per.values() for a, b, r in evs)
             latency = {"device_us_per_call_median": dev_us[len(dev_us) // 2],
                        "host_blocking_us_per_call_median": 1e6 * statistics.median(calls),
                        "calls": len(calls),
-                       "note": "device: CUDA events around one evaluation (N=1000 rows); host: the "
-                               "whole blocking NumPy call (validation, H2D, kernel, D2H)"}
+                       "note": "device: one evaluation of N=1000 rows back to back (CUDA events "
+                               "around 8 calls queued together); host: the whole blocking NumPy "
+                               "call (validation, H2D, kernel, D2H)"}
         del xh
 
     # e2e through the public API from pinned host memory (config 5)

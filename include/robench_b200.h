@@ -164,6 +164,13 @@ rb_status rb_func_evaluate_async(rb_engine* e, int32_t fn_id, int32_t precision,
 /* RB_OK or RB_E_NON_FINITE_INPUT for a completed call; RB_E_INVALID_ARGUMENT
  * once the ticket's slot was reused (4096 later calls). */
 rb_status rb_ticket_status(rb_engine* e, int64_t ticket);
+/* n_calls stream-ordered evaluations in one call (e.g. every function of the
+ * suite on one population): call i is rb_func_evaluate_async(e, fn_ids[i],
+ * precisions[i], x[i], n[i], f[i], stream, &tickets[i]).  Stops at the first
+ * argument error (its status is returned; later tickets are not written). */
+rb_status rb_func_evaluate_many(rb_engine* e, int32_t n_calls, const int32_t* fn_ids,
+                                const int32_t* precisions, const void* const* x, const int64_t* n,
+                                void* const* f, void* stream, int64_t* tickets);
 
 /* ---- one process, several GPUs ---------------------------
  * A replica of the instance pack on each device; rows are sharded

@@ -988,6 +988,35 @@ rb_status rb_func_evaluate_async(rb_engine* e, int32_t fn_id, int32_t precision,
 
 rb_status rb_ticket_status(rb_engine* e, int64_t ticket) { return ticket_status(e, ticket); }
 
+rb_status rb_func_evaluate_many(rb_engine* e, int32_t n_calls, const int32_t* fn_ids,
+                                const int32_t* precisions, const void* const* x, const int64_t* n,
+                                void* const* f, void* stream, int64_t* tickets) {
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  if (n_calls < 0 || (n_calls > 0 && (!fn_ids || !precisions || !x || !n || !f)))
+    return fail(RB_E_INVALID_ARGUMENT, "bad arguments");
+  if (n_calls > (int32_t)kFlagSlots) return fail(RB_E_INVALID_ARGUMENT, "more than 4096 calls");
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rb_status s = RB_OK;
+  for (int32_t i = 0; i < n_calls && s == RB_OK; ++i) {
+    volatile int* flag = nullptr;
+    uint32_t seq = 0;
+    if (precisions[i] == RB_DOUBLE)
+      s = launch_eval<double>(e, fn_ids[i], static_cast<const double*>(x[i]), n[i],
+                              static_cast<double*>(f[i]), st, &flag, true, &seq);
+    else if (precisions[i] == RB_SINGLE)
+      s = launch_eval<float>(e, fn_ids[i], static_cast<const float*>(x[i]), n[i],
+                             static_cast<float*>(f[i]), st, &flag, true, &seq);
+    else
+      s = fail(RB_E_INVALID_ARGUMENT, "precision must be RB_DOUBLE or RB_SINGLE");
+    if (tickets) tickets[i] = s == RB_OK ? (int64_t)seq : -1;
+  }
+  if (prev != e->device) cudaSetDevice(prev);
+  return s;
+}
+
 rb_status rb_initialize_sharded(const rb_pack* pk, int64_t max_concurrency, const int32_t* devices,
                                 int32_t n_devices, rb_sharded** out) {
   if (!out) return fail(RB_E_INVALID_ARGUMENT, "null output pointer");

@@ -209,6 +209,43 @@ class Engine:
         done.record(stream)
         return Pending(out, [(self, ticket.value)], done, keep=(pts,))
 
+    def evaluate_many(self, calls, batches, *, outs=None) -> "list[Pending]":
+        """Queue several evaluations in ONE native call (rb_func_evaluate_many):
+        ``calls`` = [(fn_id, precision), ...]; ``batches`` = {precision: CUDA
+        tensor (N x D)}, a list with one tensor per call, or one tensor;
+        ``outs`` = optional output tensors, one per call.  Same checks and
+        values as evaluate_async per call, without Python work per launch --
+        e.g. the whole suite on one population (bench.py's step)."""
+        import torch
+        if self._disposed:
+            raise UseAfterDispose("engine was disposed")
+        k = len(calls)
+        i32, i64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+        fns, precs, xs, ns, fs = (i32 * k)(), (i32 * k)(), (vp * k)(), (i64 * k)(), (vp * k)()
+        keep, results = [], []
+        for i, (fn, prec) in enumerate(calls):
+            prec = prec or self.config.precision
+            if prec not in _DTYPES:
+                raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
+            data = (batches[prec] if isinstance(batches, dict) else
+                    batches[i] if isinstance(batches, (list, tuple)) else batches)
+            if not _is_torch(data) or data.ndim != 2:
+                raise ValueError("evaluate_many takes CUDA tensor batches")
+            if data.shape[1] != self.config.dim:
+                raise DimensionMismatch(f"batch dim {data.shape[1]} != engine dim {self.config.dim}")
+            pts, out = self._device_args(data, prec, outs[i] if outs is not None else None)
+            keep.append(pts)
+            results.append(out)
+            fns[i], precs[i] = int(fn), _lib.RB_DOUBLE if prec == "double" else _lib.RB_SINGLE
+            xs[i], ns[i], fs[i] = pts.data_ptr(), pts.shape[0], out.data_ptr()
+        stream = torch.cuda.current_stream(torch.device("cuda", self.config.device))
+        tickets = (i64 * k)()
+        _lib.check(_lib.load().rb_func_evaluate_many(self._handle, k, fns, precs, xs, ns, fs,
+                                                     stream.cuda_stream, tickets))
+        done = torch.cuda.Event()
+        done.record(stream)
+        return [Pending(results[i], [(self, tickets[i])], done, keep=(keep[i],)) for i in range(k)]
+
     def ticket_status(self, ticket: int) -> None:
         """Raise NonFiniteInput if the completed call behind ``ticket`` saw a
         non-finite input (rb_ticket_status)."""

@@ -122,3 +122,25 @@ def test_two_process_sharded_engines_match_one_engine(tmp_path, world, n):
         for prec in ("double", "single"):
             assert np.array_equal(got[f"{fn}/{prec}"], one.evaluate(fn, x, precision=prec).values)
     one.dispose()
+
+
+def test_evaluate_many_matches_single_calls():
+    # one native call queueing many (function, precision) evaluations
+    # (rb_func_evaluate_many): values and statuses as one call each
+    dim = 30
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=512, seed=3))
+    x = population(dim, 300, seed=2)
+    xt = {"double": torch.from_numpy(x).cuda(), "single": torch.from_numpy(x.astype(np.float32)).cuda()}
+    calls = [(fn, p) for p in ("double", "single") for fn in FNS]
+    pend = eng.evaluate_many(calls, xt)
+    for (fn, p), pd in zip(calls, pend):
+        assert np.array_equal(pd.result().values.cpu().numpy(), eng.evaluate(fn, x, precision=p).values)
+    bad = xt["double"].clone()
+    bad[7, 1] = float("nan")
+    pend = eng.evaluate_many([(0, "double"), (20, "double")], [xt["double"], bad])
+    pend[0].result()
+    with pytest.raises(rb.NonFiniteInput):
+        pend[1].result()
+    with pytest.raises(rb.UnknownFunction):
+        eng.evaluate_many([(40, "double")], xt)
+    eng.dispose()
