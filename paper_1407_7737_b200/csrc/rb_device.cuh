@@ -1213,9 +1213,12 @@ __device__ __forceinline__ void composition_weights(const Args<T>& a, const Plan
 #pragma unroll
     for (int k = 0; k < MAX_MEMBERS; ++k)
       if (k < nm) tot = tot + w[k];
+    // w / tot as w * (1 / tot): one division per point instead of one per
+    // member (to tolerance: within an ulp of the reference's w / total)
+    const T inv = tot == T(0) ? T(0) : T(1) / tot;
 #pragma unroll
     for (int k = 0; k < MAX_MEMBERS; ++k)
-      if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;
+      if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] * inv;
   }
 }
 

@@ -113,10 +113,15 @@ def test_engine_from_files_matches_seeded(tmp_path):
     cfg = rb.EngineConfig(dim=30, max_concurrency=64, seed=2)
     a, b = rb.initialize(cfg), F.initialize_from_files(cfg, paths)
     x = np.random.default_rng(5).uniform(-100, 100, (64, 30))
+    from oracle.robench_oracle import Oracle
+    orc = Oracle(30, 2)                 # the seeded instances: pins the file engine to the reference
     for fn in (0, 10, 16, 24, 29, 36):
         for prec in ("double", "single"):
-            assert np.array_equal(a.evaluate(fn, x, precision=prec).values,
-                                  b.evaluate(fn, x, precision=prec).values)
+            got = b.evaluate(fn, x, precision=prec).values
+            assert np.array_equal(a.evaluate(fn, x, precision=prec).values, got)
+            want = orc.evaluate(fn, x, prec).astype(np.float64)
+            rel, ab = (1e-12, 1e-10) if prec == "double" else (1e-5, 0.0)
+            assert np.all(np.abs(got.astype(np.float64) - want) <= np.maximum(rel * np.abs(want), ab))
     a.dispose()
     b.dispose()
 
