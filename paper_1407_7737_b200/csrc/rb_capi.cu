@@ -23,6 +23,8 @@ extern const void* const kernels_f32[N_VARIANTS];
 extern const void* const kernels_spec_f64[FN_COUNT_SPEC];
 extern const void* const kernels_spec_f32[FN_COUNT_SPEC];
 extern const void* const fixup_f64;
+extern const void* const plan_image_f64[2];     // [MT2]
+extern const void* const plan_image_f32;
 cudaError_t set_weier_f64x(const double* a_then_c);
 cudaError_t set_weier_f32x(const float* a_then_c);
 void phase_read_f64x(unsigned long long out[8], bool reset);
@@ -151,6 +153,7 @@ struct Launch {
   int ldv = 0, max_q = 0;
   int nbuf = 1;
   int opt_rows = 0;
+  bool mt2 = false;                 // float64 DMMA units cover both m-tiles (rb_device.cuh MT2)
   size_t smem_nbuf[3] = {0, 0, 0};
 };
 
@@ -187,7 +190,8 @@ struct rb_engine {
   std::vector<int> fixup;                    // float64: bitmask of exact64 members (fixup_kernel)
   int fixup_grid = 0;
   std::vector<Launch> launch[2];
-  rb_function* d_fns = nullptr;
+  rb_function* d_fns = nullptr;              // [precision]: function records + plan images
+  rb_function* d_fns32 = nullptr;
   rb_member* d_members = nullptr;
   rb_segment* d_segments = nullptr;
   rb_group* d_groups = nullptr;
@@ -226,6 +230,7 @@ void release(rb_engine* e) {
   cudaGetDevice(&prev);
   cudaSetDevice(e->device);
   cudaFree(e->d_fns);
+  cudaFree(e->d_fns32);
   cudaFree(e->d_members);
   cudaFree(e->d_segments);
   cudaFree(e->d_groups);
@@ -256,7 +261,7 @@ rb::Args<T> make_args(const rb_engine* e, int32_t fn_id, const T* x, int64_t n, 
   a.f = f;
   a.n = n;
   a.dim = e->dim;
-  a.fns = e->d_fns;
+  a.fns = pi == 0 ? e->d_fns : e->d_fns32;
   a.members = e->d_members;
   a.segments = e->d_segments;
   a.groups = e->d_groups;
@@ -578,6 +583,8 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       Launch& L = e->launch[pi][fi];
       L.func = (pi == 0 ? rb::kernels_f64 : rb::kernels_f32)[variant[fi]];
       if (spec[fi] >= 0) L.func = (pi == 0 ? rb::kernels_spec_f64 : rb::kernels_spec_f32)[spec[fi]];
+      // must match rb::mt2_kernel<KID>() of the kernel chosen
+      L.mt2 = pi == 0 && (spec[fi] >= 0 ? fi < 29 : variant[fi] < rb::K_COUNT);
       L.max_q = std::max(max_q, 1);
       L.ldv = pi == 0 ? 0 : ldv;             // float64 has no V tile
       L.opt_rows = fn.category == RB_COMPOSITION ? fn.n_members : 0;
@@ -764,6 +771,67 @@ rb_status upload_series_constants(const rb_pack* pk) {
   return RB_OK;
 }
 
+// Per precision: the function records (the device copy's `reserved` word
+// carries the float64 exact-order members in bits 0-7 and the plan image's
+// offset in bits 8+, 16-byte units) followed by one plan image per usable
+// function, built on the device by plan_image_kernel with the very Args the
+// evaluation launches use (rb_device.cuh enter_plan).
+template <class T>
+size_t plan_bytes_host(int dim, int max_q, int opt_rows) {
+  size_t b = rb::align16(sizeof(rb::PlanHead));
+  b += 2 * rb::align16(sizeof(int) * max_q) + rb::align16(sizeof(T) * max_q);
+  if (sizeof(T) == 8) b += rb::align16(sizeof(T) * max_q);
+  b += rb::align16(sizeof(T) * opt_rows * dim);
+  return b;
+}
+
+rb_status build_function_tables(rb_engine* e, const rb_pack* pk) {
+  const int nf = pk->n_functions;
+  static const bool images = [] {
+    const char* v = std::getenv("RB_PLAN_IMAGE");
+    return !v || std::atoi(v) != 0;
+  }();
+  for (int pi = 0; pi < 2; ++pi) {
+    std::vector<rb_function> fns(pk->functions, pk->functions + nf);
+    std::vector<size_t> off(nf, 0), bytes(nf, 0);
+    size_t total = (sizeof(rb_function) * nf + 127) & ~size_t(127);
+    for (int fi = 0; fi < nf; ++fi) {
+      fns[fi].reserved = pi == 0 ? (e->fixup[fi] & 0xff) : 0;
+      const Launch& L = e->launch[pi][fi];
+      if (!images || fns[fi].category == RB_DISABLED || !L.func || !e->why[pi][fi].empty()) continue;
+      bytes[fi] = pi == 0 ? plan_bytes_host<double>(pk->dim, L.max_q, L.opt_rows)
+                          : plan_bytes_host<float>(pk->dim, L.max_q, L.opt_rows);
+      off[fi] = total;
+      total += (bytes[fi] + 127) & ~size_t(127);
+    }
+    if ((total >> 4) >= (size_t(1) << 23)) return fail(RB_E_UNSUPPORTED, "plan images too large");
+    rb_function** dst = pi == 0 ? &e->d_fns : &e->d_fns32;
+    RB_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), total));
+    // records without images first: the image kernel reads them
+    RB_CUDA(cudaMemcpy(*dst, fns.data(), sizeof(rb_function) * nf, cudaMemcpyHostToDevice));
+    for (int fi = 0; fi < nf; ++fi) {
+      if (!bytes[fi]) continue;
+      const Launch& L = e->launch[pi][fi];
+      uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(*dst) + off[fi]);
+      const void* kern = pi == 0 ? rb::plan_image_f64[L.mt2 ? 1 : 0] : rb::plan_image_f32;
+      RB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes[fi] + 1024));
+      if (pi == 0) {
+        rb::Args<double> a = make_args<double>(e, fi, nullptr, 0, nullptr, nullptr, L);
+        void* args[] = {&a, &out};
+        RB_CUDA(cudaLaunchKernel(kern, dim3(1), dim3(rb::NT), args, bytes[fi], 0));
+      } else {
+        rb::Args<float> a = make_args<float>(e, fi, nullptr, 0, nullptr, nullptr, L);
+        void* args[] = {&a, &out};
+        RB_CUDA(cudaLaunchKernel(kern, dim3(1), dim3(rb::NT), args, bytes[fi], 0));
+      }
+      fns[fi].reserved |= (int32_t)((off[fi] >> 4) << 8);
+    }
+    RB_CUDA(cudaDeviceSynchronize());
+    RB_CUDA(cudaMemcpy(*dst, fns.data(), sizeof(rb_function) * nf, cudaMemcpyHostToDevice));
+  }
+  return RB_OK;
+}
+
 // Stream-ordered call: validation now, the status later (rb_ticket_status).
 // float64 functions with exact64 members queue their fixup pass behind the
 // kernel, since nobody inspects the flags in between.
@@ -913,19 +981,13 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   e->fns.assign(pk->functions, pk->functions + pk->n_functions);
   rb_status s = plan_launches(e, pk, device);
   if (s == RB_OK) s = upload_series_constants(pk);
-  if (s == RB_OK) {
-    // the device copy's `reserved` word carries the float64 exact-order
-    // members (PlanHead::exact_mem)
-    std::vector<rb_function> fns(pk->functions, pk->functions + pk->n_functions);
-    for (int i = 0; i < pk->n_functions; ++i) fns[i].reserved = e->fixup[i];
-    s = upload(&e->d_fns, fns.data(), pk->n_functions);
-  }
   if (s == RB_OK) s = upload(&e->d_members, pk->members, pk->n_members);
   if (s == RB_OK) s = upload(&e->d_segments, pk->segments, pk->n_segments);
   if (s == RB_OK) s = upload(&e->d_groups, pk->groups, pk->n_groups);
   if (s == RB_OK) s = upload(&e->d_index, pk->index, pk->n_index);
   if (s == RB_OK) s = upload(&e->d_v64, pk->values_f64, pk->n_values);
   if (s == RB_OK) s = upload(&e->d_v32, pk->values_f32, pk->n_values);
+  if (s == RB_OK) s = build_function_tables(e, pk);
   if (s == RB_OK && cudaHostAlloc(reinterpret_cast<void**>(&e->h_flags), kSlotInts * sizeof(int) * kFlagSlots,
                                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
     s = fail(RB_E_CUDA, "mapped flag allocation failed");

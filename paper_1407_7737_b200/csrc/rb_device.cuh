@@ -289,7 +289,7 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
     P.unit_off[P.n_seg] = nu;
     // members with an exact-order path, decided by rb_initialize (plan_launches)
     // and carried in the device copy of the function record
-    P.exact_mem = sizeof(T) == 8 ? (uint32_t)P.fn.reserved : 0u;
+    P.exact_mem = sizeof(T) == 8 ? (uint32_t)P.fn.reserved & 0xffu : 0u;
   }
   __syncthreads();
   for (int mi = 0; mi < a.opt_rows && mi < P.fn.n_members; ++mi)
@@ -1213,12 +1213,11 @@ __device__ __forceinline__ void composition_weights(const Args<T>& a, const Plan
 #pragma unroll
     for (int k = 0; k < MAX_MEMBERS; ++k)
       if (k < nm) tot = tot + w[k];
-    // w / tot as w * (1 / tot): one division per point instead of one per
-    // member (to tolerance: within an ulp of the reference's w / total)
-    const T inv = tot == T(0) ? T(0) : T(1) / tot;
+    // w / tot per member: a reciprocal 1 / tot overflows when the weights are
+    // subnormal (float32 exp of a large negative argument) and 0 * inf = NaN
 #pragma unroll
     for (int k = 0; k < MAX_MEMBERS; ++k)
-      if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] * inv;
+      if (k < nm) om[k] = (tot == T(0)) ? C<T>(1.0 / nm) : w[k] / tot;
   }
 }
 
@@ -1270,12 +1269,59 @@ constexpr int min_blocks() {
   return sizeof(T) == 8 ? RB_MIN_BLOCKS_F64 : RB_MIN_BLOCKS_F32;
 }
 
+// Plan images: a function's shared-memory plan (PlanHead, the per-column and
+// per-row tables, composition optima: everything carve() places before the
+// X tile) is built once per engine and precision on the device
+// (plan_image_kernel, rb_initialize) and stored behind the function table;
+// the device copy of the function record carries its offset (bits 8+ of
+// `reserved`, 16-byte units from the table start).  Every CTA then copies
+// it in one coalesced pass instead of walking the descriptors through
+// dependent global loads (small batches: launch latency).  The kernel
+// arguments are unchanged (Args stays at 128 bytes).
+template <class T>
+__device__ __forceinline__ size_t plan_bytes(const Smem<T>& s) {
+  return (size_t)(reinterpret_cast<const unsigned char*>(s.XB[0]) -
+                  reinterpret_cast<const unsigned char*>(s.P));
+}
+
+template <class T, bool MT2>
+__device__ __forceinline__ void enter_plan(const Args<T>& a, const Smem<T>& s) {
+  const uint32_t img = (uint32_t)a.fns[a.fn].reserved >> 8;
+  if (img == 0u) {
+    load_plan<T, MT2>(a, s);
+    return;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(a.fns) +
+                                                    (size_t)img * 16);
+  uint4* dst = reinterpret_cast<uint4*>(s.P);
+  const int n16 = (int)(plan_bytes(s) / 16);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+  __syncthreads();
+  if (threadIdx.x == 0) {                  // barriers are objects, not bytes: init afresh
+    PlanHead& P = *s.P;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.mbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <class T, bool MT2>
+__global__ void __launch_bounds__(NT, 1) plan_image_kernel(const Args<T> a, uint4* out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Smem<T> s = carve<T>(smem_raw, a);
+  load_plan<T, MT2>(a, s);
+  const uint4* src = reinterpret_cast<const uint4*>(s.P);
+  const int n16 = (int)(plan_bytes(s) / 16);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
+}
+
 template <class T, int KID>
 __global__ void __launch_bounds__(NT, (min_blocks<T, KID>()))
     evaluate_kernel(const Args<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Smem<T> s = carve<T>(smem_raw, a);
-  load_plan<T, mt2_kernel<KID>()>(a, s);
+  enter_plan<T, mt2_kernel<KID>()>(a, s);
   PlanHead& P = *s.P;
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int64_t ntiles = (a.n + TP - 1) / TP;

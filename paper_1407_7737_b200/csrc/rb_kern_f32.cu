@@ -19,6 +19,9 @@ extern const void* const kernels_f32[N_VARIANTS] = {
     (const void*)evaluate_kernel<float, 20>, (const void*)evaluate_kernel<float, GENERIC>,
 };
 
+// Plan image builder (rb_device.cuh enter_plan).
+extern const void* const plan_image_f32 = (const void*)plan_image_kernel<float, false>;
+
 // Series constants of this unit's Weierstrass kernels (rb_kernels.cuh);
 // each translation unit owns its __constant__ copy.
 cudaError_t set_weier_f32(const float* a_then_c) {

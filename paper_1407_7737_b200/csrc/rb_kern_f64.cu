@@ -21,6 +21,9 @@ extern const void* const kernels_f64[N_VARIANTS] = {
 
 // The exact-order re-evaluation of marked rows (any function; float64).
 extern const void* const fixup_f64 = (const void*)fixup_kernel<double>;
+// Plan image builders (rb_device.cuh enter_plan), [MT2].
+extern const void* const plan_image_f64[2] = {(const void*)plan_image_kernel<double, false>,
+                                              (const void*)plan_image_kernel<double, true>};
 
 // Series constants of this unit's Weierstrass kernels (rb_kernels.cuh);
 // each translation unit owns its __constant__ copy.
