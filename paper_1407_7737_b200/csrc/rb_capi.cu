@@ -631,26 +631,6 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       if (pi == 0) L.nbuf = 1;           // fp64 tiles have no second X buffer
       L.smem = L.smem_nbuf[L.nbuf];
       L.grid_cap = sms * occ[L.nbuf];
-      // experiment knob: RB_OCC_COMP=p:N caps precision p's (0 = f64, 1 = f32)
-      // composition kernels at N resident CTAs per SM by padding shared memory
-      // (more L1 for the B fragments)
-      if (const char* v = std::getenv("RB_OCC_COMP")) {
-        const int want_p = std::atoi(v), want_n = std::atoi(std::strchr(v, ':') ? std::strchr(v, ':') + 1 : "0");
-        if (want_p == pi && want_n > 0 && want_n < occ[L.nbuf] &&
-            pk->functions[fi].category == RB_COMPOSITION) {
-          int per_sm = 0;
-          cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
-          const size_t padded = (size_t)(per_sm / want_n - 1024);
-          if ((int)padded <= optin && padded > L.smem) {
-            need[L.func] = std::max(need[L.func], padded);
-            cudaFuncSetAttribute(L.func, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max(padded, g_attr[std::make_pair(device, L.func)]));
-            g_attr[std::make_pair(device, L.func)] = std::max(padded, g_attr[std::make_pair(device, L.func)]);
-            L.smem = padded;
-            L.grid_cap = sms * want_n;
-          }
-        }
-      }
     }
   }
   return RB_OK;
