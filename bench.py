@@ -491,7 +491,7 @@ def run_ours(args):
     else:
         achieved = shard.count * flops[dom["fn"]] / dom["seconds"] / 1e12
         peak, unit = p_fp[dom["precision"]] / 1e12, "TFLOP/s"
-    traffic = load_json(ROOT / "profiles" / "ncu_traffic_r01.json").get(
+    traffic = load_json(ROOT / "profiles" / "r02" / "ncu_traffic.json").get(
         f"{dom['fn']}/{dom['precision']}")
     roofline = {
         "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,

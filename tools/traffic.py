@@ -1,5 +1,5 @@
 """DRAM traffic per launch of the bench's largest kernels (ncu metrics-only
-pass at the bench size), written to profiles/ncu_traffic_r01.json for
+pass at the bench size), written to profiles/r02/ncu_traffic.json for
 bench.py's roofline "traffic".  Run under gpurun:
     python tools/traffic.py 32:single 33:single 32:double 33:double"""
 import csv
@@ -26,9 +26,9 @@ for spec in sys.argv[1:]:
     if "dram__bytes_read.sum" in vals:
         out[f"{fn}/{prec}"] = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
         print(spec, vals)
-path = Path("profiles/ncu_traffic_r01.json")
+path = Path("profiles/r02/ncu_traffic.json")
 prev = json.loads(path.read_text()) if path.exists() else {}
 prev.update(out)
 path.write_text(json.dumps(prev, indent=1))
 Path("gpurun_out").mkdir(exist_ok=True)
-Path("gpurun_out/ncu_traffic_r01.json").write_text(json.dumps(prev, indent=1))
+Path("gpurun_out/ncu_traffic_r02.json").write_text(json.dumps(prev, indent=1))
