@@ -137,11 +137,13 @@ NCU_PIPES = {
 
 def ncu_pipes(fn, prec):
     """Pipe utilisation (% of peak while active) of the dominant launch from
-    its latest committed ncu --set full summary (profiles/r01/v*/), or None:
+    its latest committed ncu --set full summary (profiles/r02/ncu, else
+    profiles/r01/v*/), or None:
     the transcendental work the rotate-flop roofline leaves out."""
     import glob
-    cands = sorted(glob.glob(str(ROOT / "profiles" / "r0[12]" / "v*" / f"ncu_full_fn{fn}_{prec}.txt")),
-                   key=lambda p: (Path(p).parent.parent.name, int(Path(p).parent.name[1:])))
+    cands = sorted(glob.glob(str(ROOT / "profiles" / "r01" / "v*" / f"ncu_full_fn{fn}_{prec}.txt")),
+                   key=lambda p: int(Path(p).parent.name[1:]))
+    cands += glob.glob(str(ROOT / "profiles" / "r02" / "ncu" / f"ncu_full_fn{fn}_{prec}.txt"))
     if not cands:
         return None
     vals = {}
