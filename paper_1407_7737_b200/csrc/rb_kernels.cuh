@@ -102,37 +102,6 @@ template <class T> __device__ __forceinline__ T schwefel_g1(T w, T c10000d) {
 }
 // katsuura row sum over i = 1..32 (:178-180) for one coordinate: 8
 // accumulators in NumPy order (32 is a multiple of 8: no tail)
-template <class T> __device__ __forceinline__ T katsuura_row(T zj);
-// float64, |z| < 2^18 (every w = 2^i z below 2^51): the nearest integer by
-// the 1.5 * 2^52 shifter (two full-rate DADDs) instead of floor(w + 0.5)
-// (FRND.F64, a slow conversion-class instruction).  Equal d = |w - n|: the
-// two roundings differ only at exact ties w = k + 1/2, where d = 1/2 either
-// way; w + 0.5 and every other step are exact in this range.
-template <> __device__ __forceinline__ double katsuura_row<double>(double zj) {
-  if (!(fabs(zj) < 262144.0)) {
-    double r[8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) r[a] = 0.0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const double w = double(1ull << (i + 1)) * zj;
-      const double d = fabs(w - floor(w + 0.5));
-      r[i & 7] = fma(d, 1.0 / double(1ull << (i + 1)), r[i & 7]);
-    }
-    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  }
-  double r[8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a) r[a] = 0.0;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const double w = double(1ull << (i + 1)) * zj;
-    const double n = __dadd_rn(__dadd_rn(w, kShifter), -kShifter);
-    const double d = fabs(w - n);
-    r[i & 7] = fma(d, 1.0 / double(1ull << (i + 1)), r[i & 7]);
-  }
-  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-}
 template <class T> __device__ __forceinline__ T katsuura_row(T zj) {
   T r[8];
 #pragma unroll
