@@ -13,6 +13,8 @@
 #include <vector>
 
 #include <map>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 
 #include "rb_fnspec.cuh"
@@ -390,22 +392,88 @@ rb_status evaluate_device(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T*
 // error the contents of f are unspecified (the reference returns nothing).
 constexpr size_t kChunkBytes = size_t(32) << 20;
 
+// Persistent host worker pool for the pipeline's staging copies (spawning
+// threads per chunk cost ~0.3 ms per 32 MB chunk).  One job at a time
+// (engines serialise on the pool); the calling thread takes part.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  // fn(lo, hi) over [0, n) split into size() contiguous ranges
+  void run(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+    std::lock_guard<std::mutex> job(job_mu_);
+    const int parts = size();
+    const int64_t per = (n + parts - 1) / parts;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      per_ = per;
+      pending_ = parts - 1;
+      ++generation_;
+    }
+    cv_.notify_all();
+    fn(0, std::min(n, per));
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const char* v = std::getenv("RB_HOST_THREADS");                // staging threads (default 8)
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nt = std::min(v ? std::max(1, std::atoi(v)) : 8, hw);
+    for (int t = 1; t < nt; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int64_t, int64_t)>* fn;
+      int64_t lo, hi;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || generation_ != seen; });
+        if (stop_) return;
+        seen = generation_;
+        fn = fn_;
+        lo = t * per_;
+        hi = std::min(n_, lo + per_);
+      }
+      if (lo < hi) (*fn)(lo, hi);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int64_t, int64_t)>* fn_ = nullptr;
+  int64_t n_ = 0, per_ = 0;
+  int pending_ = 0;
+  uint64_t generation_ = 0;
+  bool stop_ = false;
+};
+
 template <class F>
 void parallel_rows(int64_t n, int64_t bytes, F&& fn) {
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  const int nt = bytes >= (int64_t(1) << 21) ? std::min(8, hw) : 1;
-  if (nt <= 1 || n < 2 * nt) {
+  if (bytes < (int64_t(1) << 21) || n < 16 || HostPool::get().size() <= 1) {
     fn(int64_t(0), n);
     return;
   }
-  std::vector<std::thread> ts;
-  const int64_t per = (n + nt - 1) / nt;
-  for (int t = 1; t < nt; ++t) {
-    const int64_t lo = t * per, hi = std::min(n, lo + per);
-    if (lo < hi) ts.emplace_back([&fn, lo, hi] { fn(lo, hi); });
-  }
-  fn(int64_t(0), std::min(n, per));
-  for (auto& th : ts) th.join();
+  const std::function<void(int64_t, int64_t)> job = fn;
+  HostPool::get().run(n, job);
 }
 
 rb_status ensure_pipeline(rb_engine* e) {
