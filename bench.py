@@ -83,7 +83,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--dim", type=int, default=100)
-    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--rows", "--n", dest="n", type=int, default=10_000_000,
+                    help="population rows N (config 5); --rows passes through torchrun unambiguously")
     ap.add_argument("--fns", default="all", help="comma list of ids (default: all 37)")
     ap.add_argument("--precisions", default="double,single")
     ap.add_argument("--no-e2e", action="store_true")

@@ -6,7 +6,7 @@
 TAG=${1:-r01}; CAPS=${2:-"32:single"}
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_$TAG.csv python bench.py --n 1000000 --steps 1 --warmup 1 \
+    --log-file gpurun_out/launches_$TAG.csv python bench.py --rows 1000000 --steps 1 --warmup 1 \
     --no-cpu --no-e2e > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launches_summary_$TAG.txt 2>&1
 first=1

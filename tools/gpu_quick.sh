@@ -4,7 +4,7 @@
 TAG=${1:-q}; CAPS=${2:-""}; N=${3:-1000000}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_$TAG.txt 2>&1
-timeout 600 python bench.py --n $N --steps 2 --warmup 1 --no-cpu --no-e2e \
+timeout 600 python bench.py --rows $N --steps 2 --warmup 1 --no-cpu --no-e2e \
     --breakdown gpurun_out/breakdown_$TAG.json > gpurun_out/bench_$TAG.txt 2>&1
 for c in $CAPS; do
   FN=${c%%:*}; PREC=${c##*:}

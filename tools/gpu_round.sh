@@ -10,7 +10,7 @@ timeout 1200 python bench.py --breakdown gpurun_out/breakdown_full_$TAG.json \
     > gpurun_out/bench_full_$TAG.txt 2> gpurun_out/bench_full_$TAG.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_$TAG.csv python bench.py --n 1000000 --steps 1 --warmup 1 \
+    --log-file gpurun_out/launches_$TAG.csv python bench.py --rows 1000000 --steps 1 --warmup 1 \
     --no-cpu --no-e2e > /dev/null 2>&1
 for c in $CAPS; do
   FN=${c%%:*}; PREC=${c##*:}
