@@ -502,6 +502,44 @@ rb_status evaluate_host_locked(rb_engine* e, int32_t fn_id, const TI* x, int64_t
   const int dim = e->dim;
   const int64_t cap = e->chunk_rows;
   const int64_t nchunks = (n + cap - 1) / cap;
+  if (nchunks == 1) {
+    // one chunk (every small batch): stage, H2D, launch, D2H on the engine
+    // stream and ONE synchronisation; the float64 exact-order pass only when
+    // the kernel marked rows (then a second D2H)
+    T* px = static_cast<T*>(e->pin_x[0]);
+    parallel_rows(n, (int64_t)sizeof(T) * n * dim, [&](int64_t lo, int64_t hi) {
+      if constexpr (std::is_same<TI, T>::value) {
+        std::memcpy(px + lo * dim, x + lo * dim, sizeof(T) * (hi - lo) * dim);
+      } else {
+        for (int64_t i = lo * dim; i < hi * dim; ++i) px[i] = static_cast<T>(x[i]);
+      }
+    });
+    RB_CUDA(cudaMemcpyAsync(e->dev_x[0], px, sizeof(T) * n * dim, cudaMemcpyHostToDevice, e->host_stream));
+    volatile int* flag = nullptr;
+    rb_status st = launch_eval<T>(e, fn_id, static_cast<const T*>(e->dev_x[0]), n,
+                                  static_cast<T*>(e->dev_f[0]), e->host_stream, &flag, false);
+    if (st != RB_OK) {
+      cudaStreamSynchronize(e->host_stream);
+      return st;
+    }
+    RB_CUDA(cudaMemcpyAsync(e->pin_f[0], e->dev_f[0], sizeof(T) * n, cudaMemcpyDeviceToHost, e->host_stream));
+    RB_CUDA(cudaStreamSynchronize(e->host_stream));
+    if (flag[0]) return non_finite();
+    if constexpr (sizeof(T) == 8) {
+      if (flag[1]) {
+        st = launch_fixup(e, fn_id, static_cast<const double*>(e->dev_x[0]), n,
+                          static_cast<double*>(e->dev_f[0]), e->host_stream,
+                          const_cast<int*>(e->d_flags + (flag - e->h_flags)));
+        if (st != RB_OK) return st;
+        RB_CUDA(cudaMemcpyAsync(e->pin_f[0], e->dev_f[0], sizeof(T) * n, cudaMemcpyDeviceToHost,
+                                e->host_stream));
+        RB_CUDA(cudaStreamSynchronize(e->host_stream));
+        if (flag[0]) return non_finite();
+      }
+    }
+    std::memcpy(f, e->pin_f[0], sizeof(T) * n);
+    return RB_OK;
+  }
   std::vector<volatile int*> flags;
   flags.reserve(nchunks);
   auto drain = [&](int64_t c) -> rb_status {   // chunk c's values into the caller's f
