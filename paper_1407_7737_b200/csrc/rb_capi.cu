@@ -18,6 +18,7 @@
 #include <thread>
 
 #include "rb_fnspec.cuh"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (no link dependency)
 
 namespace rb {
 extern const void* const kernels_f64[N_VARIANTS];
@@ -107,6 +108,14 @@ __global__ void np_powf_kernel(const float* x, const float* y, float* out, int64
 }  // namespace rb
 
 namespace {
+
+// NVTX range over a C-ABI call (tracing); ~free when no
+// tool is attached.  Shows the API boundary beside the kernels in nsys /
+// ncu --nvtx timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
@@ -1044,6 +1053,7 @@ void rb_struct_sizes(int64_t out[5]) {
 
 rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t device,
                         rb_engine** out) {
+  NvtxRange range("rb_initialize");
   if (!pk || !out) return fail(RB_E_INVALID_ARGUMENT, "null pack or output pointer");
   *out = nullptr;
   if (pk->dim < 2 || pk->n_functions <= 0 || max_concurrency < 1)
@@ -1100,24 +1110,29 @@ rb_status rb_dispose(rb_engine** engine) {
 
 rb_status rb_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64_t n, double* f,
                            void* stream) {
+  NvtxRange range("rb_func_evaluate");
   return evaluate_device<double>(e, fn_id, x, n, f, static_cast<cudaStream_t>(stream));
 }
 
 rb_status rb_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f,
                             void* stream) {
+  NvtxRange range("rb_func_evaluatef");
   return evaluate_device<float>(e, fn_id, x, n, f, static_cast<cudaStream_t>(stream));
 }
 
 rb_status rb_h_func_evaluate(rb_engine* e, int32_t fn_id, const double* x, int64_t n, double* f) {
+  NvtxRange range("rb_h_func_evaluate");
   return evaluate_host<double, double>(e, fn_id, x, n, f);
 }
 
 rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64_t n, float* f) {
+  NvtxRange range("rb_h_func_evaluatef");
   return evaluate_host<float, float>(e, fn_id, x, n, f);
 }
 
 rb_status rb_h_func_evaluate_x64(rb_engine* e, int32_t fn_id, int32_t precision, const double* x,
                                  int64_t n, void* f) {
+  NvtxRange range("rb_h_func_evaluate_x64");
   if (precision == RB_DOUBLE) return evaluate_host<double, double>(e, fn_id, x, n, static_cast<double*>(f));
   if (precision == RB_SINGLE) return evaluate_host<double, float>(e, fn_id, x, n, static_cast<float*>(f));
   return fail(RB_E_INVALID_ARGUMENT, "precision must be RB_DOUBLE or RB_SINGLE");
@@ -1125,6 +1140,7 @@ rb_status rb_h_func_evaluate_x64(rb_engine* e, int32_t fn_id, int32_t precision,
 
 rb_status rb_func_evaluate_async(rb_engine* e, int32_t fn_id, int32_t precision, const void* x,
                                  int64_t n, void* f, void* stream, int64_t* ticket) {
+  NvtxRange range("rb_func_evaluate_async");
   if (precision == RB_DOUBLE)
     return evaluate_async<double>(e, fn_id, static_cast<const double*>(x), n, static_cast<double*>(f),
                                   static_cast<cudaStream_t>(stream), ticket);
@@ -1139,6 +1155,7 @@ rb_status rb_ticket_status(rb_engine* e, int64_t ticket) { return ticket_status(
 rb_status rb_func_evaluate_many(rb_engine* e, int32_t n_calls, const int32_t* fn_ids,
                                 const int32_t* precisions, const void* const* x, const int64_t* n,
                                 void* const* f, void* stream, int64_t* tickets) {
+  NvtxRange range("rb_func_evaluate_many");
   if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
   if (n_calls < 0 || (n_calls > 0 && (!fn_ids || !precisions || !x || !n || !f)))
     return fail(RB_E_INVALID_ARGUMENT, "bad arguments");
@@ -1229,6 +1246,7 @@ rb_status rb_dispose_sharded(rb_sharded** sh) {
 rb_status rb_func_evaluate_sharded(rb_sharded* sh, int32_t fn_id, int32_t precision,
                                    const void* const* x_shards, int64_t n_total, void* const* f_full,
                                    void* const* streams, int64_t* tickets) {
+  NvtxRange range("rb_func_evaluate_sharded");
   if (!sh) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
   if (precision == RB_DOUBLE)
     return evaluate_sharded<double>(sh, fn_id, x_shards, n_total, f_full, streams, tickets);
