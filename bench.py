@@ -523,17 +523,17 @@ def run_ours(args):
     latency = None
     if not args.no_e2e and world == 1 and (args.config != 5 or args.e2e_numpy):
         xh = x64.cpu().numpy()
-        calls = []
+        call_times = []
 
         def np_step():
             for p in precs:
                 for fn in fns:
                     t0 = time.perf_counter()
                     engine.evaluate(fn, xh, p)
-                    calls.append(time.perf_counter() - t0)
+                    call_times.append(time.perf_counter() - t0)
 
         np_step()
-        calls.clear()
+        call_times.clear()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             np_step()
@@ -546,11 +546,29 @@ def run_ours(args):
                      "path": ("Engine.evaluate(fn, numpy float64 X, precision) -> rb_h_func_evaluate[f]; "
                               "float32 calls cast X on the host first, as the reference does (engine.py:201)"),
                      "timing": "host wall clock around the blocking calls"}
+        # the same step through the many-call host API: one population, every
+        # (function, precision) in ONE call (rb_h_func_evaluate_many): the
+        # rows cross PCIe once per step instead of once per call
+        if args.config == 5:
+            engine.evaluate_many(calls, xh)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                engine.evaluate_many(calls, xh)
+            wall_m = time.perf_counter() - t0
+            e2e_numpy["many_call"] = {
+                "value": args.steps * len(calls) * args.n / wall_m, "unit": UNIT,
+                "h2d_bytes_per_step": shard.count * D * 8,
+                "d2h_bytes_per_step": sum(shard.count * (8 if p == "double" else 4) for _, p in calls),
+                "ms_per_step": 1e3 * wall_m / args.steps,
+                "path": ("Engine.evaluate_many([(fn, precision) ...], numpy float64 X) -> "
+                         "rb_h_func_evaluate_many: X uploaded once per ~32 MB row chunk for all "
+                         "calls, float32 cast on the device"),
+                "timing": "host wall clock around the blocking call"}
         if args.config == 1:
             dev_us = sorted(1e3 * a.elapsed_time(b) / r for evs in per.values() for a, b, r in evs)
             latency = {"device_us_per_call_median": dev_us[len(dev_us) // 2],
-                       "host_blocking_us_per_call_median": 1e6 * statistics.median(calls),
-                       "calls": len(calls),
+                       "host_blocking_us_per_call_median": 1e6 * statistics.median(call_times),
+                       "calls": len(call_times),
                        "note": "device: one evaluation of N=1000 rows back to back (CUDA events "
                                "around 8 calls queued together); host: the whole blocking NumPy "
                                "call (validation, H2D, kernel, D2H)"}

@@ -150,6 +150,16 @@ rb_status rb_h_func_evaluatef(rb_engine* e, int32_t fn_id, const float* x, int64
 rb_status rb_h_func_evaluate_x64(rb_engine* e, int32_t fn_id, int32_t precision, const double* x,
                                  int64_t n, void* f);
 
+/* Many (fn_ids[i], precisions[i]) evaluations of ONE host population of
+ * float64 rows, synchronous: the rows cross PCIe once (per ~32 MB chunk) for
+ * all calls instead of once per call; single-precision calls evaluate
+ * float32(x) (engine.py:201).  f[i]: n values (double* or float*).  Every
+ * call is validated (the reference's order) before any work; a non-finite x
+ * returns RB_E_NON_FINITE_INPUT (f unspecified).  At most 1024 calls. */
+rb_status rb_h_func_evaluate_many(rb_engine* e, int32_t n_calls, const int32_t* fn_ids,
+                                  const int32_t* precisions, const double* x, int64_t n,
+                                  void* const* f);
+
 /* ---- stream-ordered calls with a deferred status ------------------------ */
 /* Enqueue the evaluation on `stream` and return at once: argument errors
  * (the reference's validation order) come back now; the input's finiteness

@@ -37,7 +37,7 @@ EXPORTS = ("rb_initialize", "rb_dispose", "rb_func_evaluate", "rb_func_evaluatef
            "rb_debug_phases", "rb_uniform_population", "rb_func_evaluate_async",
            "rb_ticket_status", "rb_initialize_sharded", "rb_func_evaluate_sharded",
            "rb_sharded_ticket_status", "rb_dispose_sharded", "rb_h_func_evaluate_x64",
-           "rb_func_evaluate_many")
+           "rb_func_evaluate_many", "rb_h_func_evaluate_many")
 RB_DOUBLE, RB_SINGLE = 0, 1
 
 
@@ -93,6 +93,9 @@ def load() -> ctypes.CDLL:
                                           ctypes.POINTER(vp), ctypes.POINTER(i64), ctypes.POINTER(vp),
                                           vp, ctypes.POINTER(i64)]
     lib.rb_func_evaluate_many.restype = i32
+    lib.rb_h_func_evaluate_many.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp, i64,
+                                            ctypes.POINTER(vp)]
+    lib.rb_h_func_evaluate_many.restype = i32
     lib.rb_h_func_evaluate_x64.restype = i32
     lib.rb_ticket_status.argtypes = [vp, i64]
     lib.rb_initialize_sharded.argtypes = [ctypes.POINTER(RbPack), i64, ctypes.POINTER(i32), i32,
@@ -103,7 +106,7 @@ def load() -> ctypes.CDLL:
     lib.rb_dispose_sharded.argtypes = [ctypes.POINTER(vp)]
     for name in ("rb_func_evaluate_async", "rb_ticket_status", "rb_initialize_sharded",
                  "rb_func_evaluate_sharded", "rb_sharded_ticket_status", "rb_dispose_sharded", "rb_h_func_evaluate_x64",
-           "rb_func_evaluate_many"):
+           "rb_func_evaluate_many", "rb_h_func_evaluate_many"):
         getattr(lib, name).restype = i32
     _check_layout(lib)
     _lib = lib

@@ -210,15 +210,21 @@ class Engine:
         return Pending(out, [(self, ticket.value)], done, keep=(pts,))
 
     def evaluate_many(self, calls, batches, *, outs=None) -> "list[Pending]":
-        """Queue several evaluations in ONE native call (rb_func_evaluate_many):
-        ``calls`` = [(fn_id, precision), ...]; ``batches`` = {precision: CUDA
-        tensor (N x D)}, a list with one tensor per call, or one tensor;
+        """Several evaluations in ONE native call: ``calls`` = [(fn_id,
+        precision), ...].  Host rows (a NumPy array / PointBatch): returns
+        [EvalResult] synchronously, the rows crossing PCIe once for all calls
+        (rb_h_func_evaluate_many; float32 calls evaluate float32(X) as
+        engine.py:201).  CUDA tensors (rb_func_evaluate_many): ``batches`` =
+        {precision: tensor (N x D)}, a list with one tensor per call, or one
+        tensor;
         ``outs`` = optional output tensors, one per call.  Same checks and
         values as evaluate_async per call, without Python work per launch --
         e.g. the whole suite on one population (bench.py's step)."""
-        import torch
         if self._disposed:
             raise UseAfterDispose("engine was disposed")
+        if not isinstance(batches, (dict, list, tuple)) and not _is_torch(batches):
+            return self._evaluate_many_host(calls, batches)
+        import torch
         k = len(calls)
         i32, i64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
         fns, precs, xs, ns, fs = (i32 * k)(), (i32 * k)(), (vp * k)(), (i64 * k)(), (vp * k)()
@@ -245,6 +251,31 @@ class Engine:
         done = torch.cuda.Event()
         done.record(stream)
         return [Pending(results[i], [(self, tickets[i])], done, keep=(keep[i],)) for i in range(k)]
+
+    def _evaluate_many_host(self, calls, batch) -> "list[EvalResult]":
+        """Host rows (NumPy / PointBatch): every call's values, the rows
+        crossing PCIe once for all calls (rb_h_func_evaluate_many)."""
+        if not isinstance(batch, PointBatch):
+            batch = PointBatch(batch.data if hasattr(batch, "data") and not isinstance(batch, np.ndarray)
+                               else batch)
+        if batch.dim != self.config.dim:
+            raise DimensionMismatch(f"batch dim {batch.dim} != engine dim {self.config.dim}")
+        pts = np.ascontiguousarray(batch.data, dtype=np.float64)
+        k = len(calls)
+        i32, vp = ctypes.c_int32, ctypes.c_void_p
+        fns, precs, fs = (i32 * k)(), (i32 * k)(), (vp * k)()
+        outs = []
+        for i, (fn, prec) in enumerate(calls):
+            prec = prec or self.config.precision
+            if prec not in _DTYPES:
+                raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
+            out = np.empty(pts.shape[0], dtype=_DTYPES[prec])
+            outs.append(out)
+            fns[i], precs[i] = int(fn), _lib.RB_DOUBLE if prec == "double" else _lib.RB_SINGLE
+            fs[i] = out.ctypes.data
+        _lib.check(_lib.load().rb_h_func_evaluate_many(self._handle, k, fns, precs, _lib.ptr(pts),
+                                                       pts.shape[0], fs))
+        return [EvalResult(o) for o in outs]
 
     def ticket_status(self, ticket: int) -> None:
         """Raise NonFiniteInput if the completed call behind ``ticket`` saw a

@@ -123,3 +123,25 @@ def test_host_pipeline_chunks_match_the_device_path():
         with pytest.raises(rb.NonFiniteInput):
             eng.evaluate(0, bad, precision=prec)
     eng.dispose()
+
+
+def test_host_evaluate_many_matches_single_calls():
+    # one host population, many functions: rows uploaded once per chunk
+    # (rb_h_func_evaluate_many; ~128 MB chunks = 167 772 rows at D=100: 2 chunks)
+    dim, n = 100, 200_003
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=n, seed=1))
+    x = population(dim, n, seed=3)
+    from paper_1407_7737_b200 import instances
+    x[180_000] = instances.build(21, dim, 1).shift         # an exact-order fixup row (chunk 2)
+    calls = [(fn, p) for p in ("double", "single") for fn in (0, 8, 21, 24, 33)]
+    res = eng.evaluate_many(calls, x)
+    for (fn, p), r in zip(calls, res):
+        assert np.array_equal(r.values, eng.evaluate(fn, x, precision=p).values), (fn, p)
+    assert res[2].values[180_000] == 100.0
+    bad = x.copy()
+    bad[n - 1, 0] = np.inf
+    with pytest.raises(rb.NonFiniteInput):
+        eng.evaluate_many(calls, bad)
+    with pytest.raises(rb.UnknownFunction):
+        eng.evaluate_many([(0, "double"), (99, "single")], x)
+    eng.dispose()
