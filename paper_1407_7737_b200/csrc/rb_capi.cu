@@ -1065,7 +1065,14 @@ rb_status build_function_tables(rb_engine* e, const rb_pack* pk) {
       const Launch& L = e->launch[pi][fi];
       uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(*dst) + off[fi]);
       const void* kern = pi == 0 ? rb::plan_image_f64[L.mt2 ? 1 : 0] : rb::plan_image_f32;
-      RB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes[fi] + 1024));
+      {                                      // only ever raised (engines coexist)
+        std::lock_guard<std::mutex> lock(g_attr_mu);
+        size_t& have = g_attr[std::make_pair(e->device, kern)];
+        if (bytes[fi] > have) {
+          RB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes[fi]));
+          have = bytes[fi];
+        }
+      }
       if (pi == 0) {
         rb::Args<double> a = make_args<double>(e, fi, nullptr, 0, nullptr, nullptr, L);
         void* args[] = {&a, &out};

@@ -145,3 +145,33 @@ def test_host_evaluate_many_matches_single_calls():
     with pytest.raises(rb.UnknownFunction):
         eng.evaluate_many([(0, "double"), (99, "single")], x)
     eng.dispose()
+
+
+def test_two_engines_from_threads_share_the_staging_pool():
+    # the host pipeline's worker pool is process-wide: engines of different
+    # dims called from several threads at once give the single-thread values
+    import threading
+    engs = [rb.initialize(rb.EngineConfig(dim=d, max_concurrency=200_000, seed=1)) for d in (30, 100)]
+    xs = [population(d, 150_000, seed=d) for d in (30, 100)]
+    want = [[e.evaluate(fn, x, precision=p).values for fn in (0, 21, 33) for p in ("double", "single")]
+            for e, x in zip(engs, xs)]
+    got, errs = [None, None, None, None], []
+
+    def run(i):
+        try:
+            e, x = engs[i % 2], xs[i % 2]
+            got[i] = [e.evaluate(fn, x, precision=p).values for fn in (0, 21, 33) for p in ("double", "single")]
+        except Exception as ex:           # pragma: no cover - reported below
+            errs.append(ex)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(4):
+        for a, b in zip(got[i], want[i % 2]):
+            assert np.array_equal(a, b)
+    for e in engs:
+        e.dispose()
