@@ -28,6 +28,8 @@ extern const void* const kernels_spec_f32[FN_COUNT_SPEC];
 extern const void* const fixup_f64;
 extern const void* const plan_image_f64[2];     // [MT2]
 extern const void* const plan_image_f32;
+extern const void* const big_f64;
+extern const void* const big_f32;
 cudaError_t set_weier_f64x(const double* a_then_c);
 cudaError_t set_weier_f32x(const float* a_then_c);
 void phase_read_f64x(unsigned long long out[8], bool reset);
@@ -172,8 +174,17 @@ struct Launch {
   int nbuf = 1;
   int opt_rows = 0;
   bool mt2 = false;                 // float64 DMMA units cover both m-tiles (rb_device.cuh MT2)
+  bool big = false;                 // evaluate_big_kernel: tiles in global scratch (per_cta bytes per CTA)
+  size_t per_cta = 0;
   size_t smem_nbuf[3] = {0, 0, 0};
 };
+
+// RB_BIG=1 serves every function with evaluate_big_kernel (tests: the
+// large-dimension path at dimensions whose tiles fit).
+int big_mode() {
+  const char* v = std::getenv("RB_BIG");
+  return v ? std::atoi(v) : 0;
+}
 
 // RB_PREFETCH=0/1 forces single / double X buffering (default: auto).
 int prefetch_mode() {
@@ -374,6 +385,19 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
   rb::Args<T> a = make_args<T>(e, fn_id, x, n, f, dflag, L);
   const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
+  if (L.big) {
+    // per-CTA tiles in stream-ordered scratch (the pool caches it across calls)
+    unsigned char* scratch = nullptr;
+    size_t per_cta = L.per_cta;
+    RB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), per_cta * grid, stream));
+    void* args[] = {&a, &scratch, &per_cta};
+    const cudaError_t err = cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream);
+    cudaFreeAsync(scratch, stream);
+    RB_CUDA(err);
+    g_launches.fetch_add(1);
+    *flag_out = hflag;
+    return RB_OK;
+  }
   void* args[] = {&a};
   RB_CUDA(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream));
   g_launches.fetch_add(1);
@@ -831,10 +855,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       ldv = std::max(ldv, q4);
       if (exact64 && !deep) e->fixup[fi] |= 1 << mi;   // (deep: float64 keeps the DMMA z)
     }
-    if (units > rb::MAX_UNITS) {
-      e->why[0][fi] = e->why[1][fi] = "exceeds the DMMA unit table";
-      continue;
-    }
+    const bool many_units = units > rb::MAX_UNITS;   // -> evaluate_big_kernel (on-the-fly units)
     if (fn.category == RB_BASIC && fn.n_members == 1 && first.n_segments == 1)
       variant[fi] = pk->segments[s0].kernel;
     if (fi >= rb::FN_FIRST_SPEC && fi < rb::FN_FIRST_SPEC + rb::FN_COUNT_SPEC) {
@@ -862,11 +883,16 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       for (int nb = 1; nb <= 2; ++nb)
         L.smem_nbuf[nb] = pi == 0 ? rb::smem_bytes<double>(pk->dim, L.ldv, e->ldz[0], L.max_q, nb, L.opt_rows)
                                   : rb::smem_bytes<float>(pk->dim, L.ldv, e->ldz[1], L.max_q, nb, L.opt_rows);
-      if ((int)L.smem_nbuf[1] > optin) {
-        e->why[pi][fi] = "dimension " + std::to_string(pk->dim) + " needs " +
-                         std::to_string(L.smem_nbuf[1]) + " bytes of shared memory per tile (limit " +
-                         std::to_string(optin) + ")";
-        L.func = nullptr;
+      if ((int)L.smem_nbuf[1] > optin || (pi == 0 && many_units) || big_mode() == 1) {
+        // the tile does not fit: PlanHead in shared memory, the rest in a
+        // per-CTA slice of global scratch (evaluate_big_kernel)
+        L.big = true;
+        L.mt2 = false;
+        L.nbuf = 1;
+        L.func = pi == 0 ? rb::big_f64 : rb::big_f32;
+        L.smem = rb::align16(sizeof(rb::PlanHead));
+        L.per_cta = L.smem_nbuf[1] - L.smem;
+        need[L.func] = std::max(need[L.func], L.smem);
         continue;
       }
       const size_t top = (int)L.smem_nbuf[2] <= optin ? L.smem_nbuf[2] : L.smem_nbuf[1];
@@ -889,6 +915,15 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
       Launch& L = e->launch[pi][fi];
       if (!L.func) continue;
       int occ[3] = {0, 0, 0};
+      if (L.big) {
+        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], L.func, rb::NT, L.smem));
+        if (occ[1] < 1) {
+          e->why[pi][fi] = "kernel does not fit on an SM";
+          continue;
+        }
+        L.grid_cap = sms * std::min(occ[1], 2);     // bounds the scratch (per_cta each)
+        continue;
+      }
       for (int nb = 1; nb <= 2; ++nb)
         if ((int)L.smem_nbuf[nb] <= optin)
           RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[nb], L.func, rb::NT,
@@ -1049,7 +1084,8 @@ rb_status build_function_tables(rb_engine* e, const rb_pack* pk) {
     for (int fi = 0; fi < nf; ++fi) {
       fns[fi].reserved = pi == 0 ? (e->fixup[fi] & 0xff) : 0;
       const Launch& L = e->launch[pi][fi];
-      if (!images || fns[fi].category == RB_DISABLED || !L.func || !e->why[pi][fi].empty()) continue;
+      if (!images || fns[fi].category == RB_DISABLED || !L.func || L.big || !e->why[pi][fi].empty())
+        continue;
       bytes[fi] = pi == 0 ? plan_bytes_host<double>(pk->dim, L.max_q, L.opt_rows)
                           : plan_bytes_host<float>(pk->dim, L.max_q, L.opt_rows);
       off[fi] = total;

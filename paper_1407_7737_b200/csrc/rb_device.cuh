@@ -77,6 +77,9 @@ constexpr int NTC = 2;          // DMMA n-tiles (8 rows) sharing one A fragment 
                                 // (3 measured: +1-3% basic, -10-18% compositions: spills)
 constexpr int GENERIC = -1;     // kernel template id for hybrids / compositions
 constexpr int FIXUP = -2;       // member_value mode of fixup_kernel (exact-order float64)
+constexpr int BIGDIM = -3;      // member_value mode of evaluate_big_kernel (tiles in global memory)
+// modes that evaluate exact64 members in NumPy's order directly (no marks)
+__host__ __device__ constexpr bool exact_mode(int kid) { return kid == FIXUP || kid == BIGDIM; }
 
 // Kernel arguments: 128 bytes.  Measured: 4-16 more bytes (unused) cost
 // the float64 composition kernels 8-16 % at N = 10^7 (code generation), so
@@ -194,12 +197,15 @@ __host__ __device__ inline size_t smem_bytes(int dim, int ldv, int ldz, int max_
   return b;
 }
 
+// plan_base: the PlanHead (shared memory); rest: everything after it --
+// shared memory as well, or for the large-dimension kernel a per-CTA slice
+// of global scratch (evaluate_big_kernel)
 template <class T>
-__device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
+__device__ inline Smem<T> carve2(unsigned char* plan_base, unsigned char* rest, const Args<T>& a) {
   Smem<T> s;
+  s.P = reinterpret_cast<PlanHead*>(plan_base);
+  unsigned char* base = rest;
   size_t off = 0;
-  s.P = reinterpret_cast<PlanHead*>(base);
-  off += align16(sizeof(PlanHead));
   s.qsrc = reinterpret_cast<int*>(base + off);
   off += align16(sizeof(int) * a.max_q);
   s.prow = reinterpret_cast<int*>(base + off);
@@ -225,6 +231,11 @@ __device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
   if (sizeof(T) == 4) off += align16(sizeof(T) * TP * a.ldv);
   s.ZS = reinterpret_cast<T*>(base + off);
   return s;
+}
+
+template <class T>
+__device__ inline Smem<T> carve(unsigned char* base, const Args<T>& a) {
+  return carve2<T>(base, base + align16(sizeof(PlanHead)), a);
 }
 
 __device__ __forceinline__ int round4(int v) { return (v + 3) & ~3; }
@@ -512,18 +523,39 @@ __device__ __forceinline__ void dmma_run_mt2(const double* X0, const double* X1,
   }
 }
 
-template <int NW, bool CHECK, bool MT2>
+// BIG (evaluate_big_kernel): the units of plan segments [s_first, s_end)
+// are enumerated on the fly (group-major, as load_plan's table) instead of
+// read from the fixed-size PlanHead table
+__device__ __forceinline__ uint32_t unit_at(const PlanHead& P, int g, int u) {
+  for (;;) {
+    const int cnt = (TP / 16) * ((P.grp[g].m + 7) >> 3);
+    if (u < cnt) break;
+    u -= cnt;
+    ++g;
+  }
+  const int ntn = (P.grp[g].m + 7) >> 3;
+  return (uint32_t)g | ((uint32_t)(u / ntn) << 8) | ((uint32_t)(u % ntn) << 16);
+}
+
+template <int NW, bool CHECK, bool MT2, bool BIG = false>
 __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>& s, int s_first,
                                       int s_end, int warp) {
   const PlanHead& P = *s.P;
   const int lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int u0 = P.unit_off[s_first];
-  const int total = P.unit_off[s_end] - u0;
+  int u0 = 0, total = 0;
+  const int gb = P.seg[s_first].group0 - P.grp_base;
+  if constexpr (BIG) {
+    const int ge = P.seg[s_end - 1].group0 + P.seg[s_end - 1].n_groups - P.grp_base;
+    for (int g = gb; g < ge; ++g) total += (TP / 16) * ((P.grp[g].m + 7) >> 3);
+  } else {
+    u0 = P.unit_off[s_first];
+    total = P.unit_off[s_end] - u0;
+  }
   const int end = (warp + 1) * total / NW;
   uint32_t nf = 0u;
   for (int u = warp * total / NW; u < end;) {
-    const uint32_t ud = P.unit[u0 + u];
+    const uint32_t ud = BIG ? unit_at(P, gb, u) : P.unit[u0 + u];
     const int g = ud & 0xff, mt = (ud >> 8) & 0xff, nt0 = ud >> 16;
     const rb_group& G = P.grp[g];
     const int m = G.m, ntn = (m + 7) >> 3, nks = (m + 3) >> 2;
@@ -558,10 +590,10 @@ __device__ inline uint32_t rotate_f64(const Args<double>& a, const Smem<double>&
 }
 
 // z of plan segments [s_first, s_end) (the chunks of one member, side by side)
-template <bool CHECK, bool MT2 = false>
+template <bool CHECK, bool MT2 = false, bool BIG = false>
 __device__ inline uint32_t rotate(const Args<double>& a, const Smem<double>& s, int s_first,
                                   int s_end) {
-  return rotate_f64<NWARPS, CHECK, MT2>(a, s, s_first, s_end, threadIdx.x >> 5);
+  return rotate_f64<NWARPS, CHECK, MT2, BIG>(a, s, s_first, s_end, threadIdx.x >> 5);
 }
 
 // ------------------------------------------------------------ rotate fp32
@@ -705,7 +737,7 @@ __device__ __forceinline__ void f32_leaf(const float4* Vq, const float* bp, int 
 }
 
 // the V tile is in place (gather_v + barrier)
-template <bool CHECK, bool MT2 = false>
+template <bool CHECK, bool MT2 = false, bool BIG = false>
 __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, int s_first,
                                   int s_end) {
   const PlanHead& P = *s.P;
@@ -1032,7 +1064,7 @@ __device__ __forceinline__ void issue_next_x(const Args<T>& a, const Smem<T>& s,
 // where z lives (row stride ldz).
 // EXACT (float64, fixup_kernel): members with an exact-order path
 // (P.exact_mem) rotate in NumPy's order instead of by DMMA.
-template <class T, bool EXACT = false, bool MT2 = false>
+template <class T, bool EXACT = false, bool MT2 = false, bool BIG = false>
 __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_member& mem,
                                  TileCtx& t) {
   const PlanHead& P = *s.P;
@@ -1069,7 +1101,8 @@ __device__ const T* stage_member(const Args<T>& a, const Smem<T>& s, const rb_me
         nf = t.check_z ? rotate_exact_f64<true>(a, s, mem, s_first, s_end)
                        : rotate_exact_f64<false>(a, s, mem, s_first, s_end);
       else
-        nf = t.check_z ? rotate<true>(a, s, s_first, s_end) : rotate<false>(a, s, s_first, s_end);
+        nf = t.check_z ? rotate<true, false, BIG>(a, s, s_first, s_end)
+                       : rotate<false, false, BIG>(a, s, s_first, s_end);
     } else {
       nf = t.check_z ? rotate<true, MT2>(a, s, s_first, s_end) : rotate<false, MT2>(a, s, s_first, s_end);
     }
@@ -1092,7 +1125,7 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
   const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const PlanHead& P = *s.P;
   RB_PHASE_MARK(c0);
-  const T* zb = stage_member<T, KID == FIXUP, mt2_kernel<KID>()>(a, s, mem, t);
+  const T* zb = stage_member<T, exact_mode(KID), mt2_kernel<KID>(), KID == BIGDIM>(a, s, mem, t);
   if (last) issue_next_x(a, s, t);
   RB_PHASE_MARK(c1);
   // compile-time: can this kernel meet a float64 exact64 member at all?
@@ -1104,7 +1137,7 @@ __device__ T member_value(const Args<T>& a, const Smem<T>& s, const rb_member& m
     const Pt<T> pt{zb + p * a.ldz + seg.src, seg.d, l8, a.values + seg.ctab, mark};
     T v;
     if constexpr (KID >= 0) v = kernel_value_k<T, KID>(pt);
-    else v = kernel_value<T, KID == FIXUP>(seg.kernel, pt);
+    else v = kernel_value<T, exact_mode(KID)>(seg.kernel, pt);
     total = (si == 0) ? v : total + v;
   }
   __syncthreads();                      // z is rewritten by the next member / tile
@@ -1251,7 +1284,7 @@ __device__ T composition_value(const Args<T>& a, const Smem<T>& s, TileCtx& t, b
     t.live = P.livek[k];
     if (!t.live) continue;
     const rb_member& mem = P.mem[k];
-    const T g = member_value<T, MODE>(a, s, mem, t, MODE != FIXUP && k == nm - 1, ill);
+    const T g = member_value<T, MODE>(a, s, mem, t, !exact_mode(MODE) && k == nm - 1, ill);
     if (omk != T(0)) total = total + omk * ((T)mem.height * g + (T)mem.bias);
   }
   return total;
@@ -1483,6 +1516,56 @@ __global__ void __launch_bounds__(NT, 1) fixup_kernel(const Args<T> a) {
     const T result = P.fn.category == RB_COMPOSITION ? composition_value<T, FIXUP>(a, s, t, valid)
                                                      : member_value<T, FIXUP>(a, s, P.mem[0], t, false);
     if (l8 == 0 && valid) a.f[row0 + (int)__fns(marked, 0, p + 1)] = result + C<T>(100.0);
+    __syncthreads();
+  }
+}
+
+// Dimensions whose tile does not fit in shared memory (or whose DMMA units
+// overflow the PlanHead table): the same evaluation with only the PlanHead
+// in shared memory and the per-column tables, optima, X / V / z tiles in a
+// per-CTA slice of global scratch (`per_cta` bytes from `scratch`, carve2),
+// served by L1 / L2.  Tiles are loaded with plain coalesced loads; float64
+// exact64 members rotate in NumPy's order directly (no marks, no fixup
+// pass); DMMA units are enumerated on the fly (unit_at).  Values equal the
+// shared-memory kernels' (float32: bit-identical; float64: the fixup pass's
+// values for every row).
+template <class T>
+__global__ void __launch_bounds__(NT, 1)
+    evaluate_big_kernel(const Args<T> a, unsigned char* scratch, size_t per_cta) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Smem<T> s = carve2<T>(smem_raw, scratch + (size_t)blockIdx.x * per_cta, a);
+  load_plan(a, s);
+  PlanHead& P = *s.P;
+  const int p = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const int64_t ntiles = (a.n + TP - 1) / TP;
+  TileCtx t{0, 0, 0u, false, true, 0u, false};
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * TP;
+    const int nv = tile_rows(a, tile);
+    const T* src = a.x + row0 * a.dim;
+    for (int64_t e = threadIdx.x; e < (int64_t)nv * a.dim; e += NT) s.XS[e] = src[e];
+    const uint32_t valid_mask = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
+    if (threadIdx.x == 0) {
+      P.live = valid_mask;
+#pragma unroll
+      for (int k = 0; k < MAX_MEMBERS; ++k) P.livek[k] = 0u;
+    }
+    __syncthreads();
+    const bool valid = p < nv;
+    t.tile = tile;
+    t.nv = nv;
+    t.live = valid_mask;
+    uint32_t mx = 0u;                          // X scan as in evaluate_kernel
+    if (valid) {
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(s.XS + p * a.dim);
+      constexpr int W = sizeof(T) / 4;
+      for (int j = l8; j < a.dim; j += 8) mx = max(mx, xw[j * W + W - 1] & 0x7fffffffu);
+    }
+    if (sizeof(T) == 8 ? mx >= 0x7ff00000u : mx >= 0x7f800000u) raise_flag(a);
+    t.check_z = __syncthreads_or(sizeof(T) == 8 ? mx >= 0x7bf00000u : mx >= 0x71800000u) != 0;
+    const T result = P.fn.category == RB_COMPOSITION ? composition_value<T, BIGDIM>(a, s, t, valid)
+                                                     : member_value<T, BIGDIM>(a, s, P.mem[0], t, false);
+    if (l8 == 0 && valid) a.f[row0 + p] = result + C<T>(100.0);    // engine.py:209
     __syncthreads();
   }
 }

@@ -19,6 +19,8 @@ extern const void* const kernels_f32[N_VARIANTS] = {
     (const void*)evaluate_kernel<float, 20>, (const void*)evaluate_kernel<float, GENERIC>,
 };
 
+// Large dimensions: tiles in global scratch (rb_device.cuh evaluate_big_kernel).
+extern const void* const big_f32 = (const void*)evaluate_big_kernel<float>;
 // Plan image builder (rb_device.cuh enter_plan).
 extern const void* const plan_image_f32 = (const void*)plan_image_kernel<float, false>;
 

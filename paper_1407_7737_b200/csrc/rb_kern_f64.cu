@@ -21,6 +21,8 @@ extern const void* const kernels_f64[N_VARIANTS] = {
 
 // The exact-order re-evaluation of marked rows (any function; float64).
 extern const void* const fixup_f64 = (const void*)fixup_kernel<double>;
+// Large dimensions: tiles in global scratch (rb_device.cuh evaluate_big_kernel).
+extern const void* const big_f64 = (const void*)evaluate_big_kernel<double>;
 // Plan image builders (rb_device.cuh enter_plan), [MT2].
 extern const void* const plan_image_f64[2] = {(const void*)plan_image_kernel<double, false>,
                                               (const void*)plan_image_kernel<double, true>};
