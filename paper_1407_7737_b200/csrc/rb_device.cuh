@@ -1544,6 +1544,8 @@ __global__ void __launch_bounds__(NT, 1)
     const int nv = tile_rows(a, tile);
     const T* src = a.x + row0 * a.dim;
     for (int64_t e = threadIdx.x; e < (int64_t)nv * a.dim; e += NT) s.XS[e] = src[e];
+    // rows past a ragged end: defined values (the DMMA tiles read all 32)
+    for (int64_t e = (int64_t)nv * a.dim + threadIdx.x; e < (int64_t)TP * a.dim; e += NT) s.XS[e] = T(0);
     const uint32_t valid_mask = nv == 32 ? 0xffffffffu : ((1u << nv) - 1u);
     if (threadIdx.x == 0) {
       P.live = valid_mask;
