@@ -37,7 +37,13 @@ def _is_torch(x) -> bool:
 
 @dataclass(frozen=True)
 class EngineConfig:
-    """engine.py:34-52, plus ``device``."""
+    """engine.py:34-52, plus ``device``.
+
+    ``dim``: any value >= 2, as in the reference (engine.py:42-44).  Up to
+    D ~ 340 every function runs from shared-memory tiles.  Past that, the
+    functions whose tile no longer fits use the large-dimension kernel
+    (tiles in global scratch).  That kernel is slower
+    but gives the same values."""
 
     dim: int
     max_concurrency: int = 50
