@@ -623,14 +623,24 @@ __device__ inline uint32_t gather_v(const Args<float>& a, const Smem<float>& s, 
     const int kp = round4(P.grp[g0 + g].m);
     const int* qs = s.qsrc + P.gq0[g0 + g];
     const float* qo = s.qo + P.gq0[g0 + g];
-#pragma unroll 4
-    for (int e = threadIdx.x; e < TP * kp; e += NT) {
-      const int q = e / TP, p = e - q * TP;
-      const float x = s.XS[p * a.dim + qs[q]];
-      if (p < nv) mx = max(mx, __float_as_uint(x) & 0x7fffffffu);
-      float v = scale * (x - qo[q]);
-      if (pre != 0.0f) v = v + pre;
-      s.VS[(vq + q) * TP + vslot(p)] = v;
+    // item (q, p0): points p0 + 8i (i < 4), which vslot places side by side:
+    // one float4 store, one column-table read for four elements
+    for (int e = threadIdx.x; e < (TP / 4) * kp; e += NT) {
+      const int q = e >> 3, p0 = e & 7;
+      const int src = qs[q];
+      const float o = qo[q];
+      float4 v4;
+      float* v = reinterpret_cast<float*>(&v4);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int p = p0 + 8 * i;
+        const float x = s.XS[p * a.dim + src];
+        if (p < nv) mx = max(mx, __float_as_uint(x) & 0x7fffffffu);
+        float t = scale * (x - o);
+        if (pre != 0.0f) t = t + pre;
+        v[i] = t;
+      }
+      *reinterpret_cast<float4*>(s.VS + (vq + q) * TP + p0 * 4) = v4;
     }
     vq += kp;
   }
