@@ -147,6 +147,8 @@ struct PlanHead {
   int unit_off[MAX_SEGMENTS + 1];  // fp64 rotate: segment si's units are unit[unit_off[si] ..)
   uint32_t exact_mem;             // fp64: members with an exact-order path (exact64_kernel)
   uint32_t marked;                // fixup_kernel: marked points of the current chunk
+  int icum[MAX_GROUPS + 1];       // fp32 rotate: items (4 points x 4 rows) before plan group g
+  int vcum[MAX_GROUPS + 1];       // fp32: V rows (4-padded group sizes) before plan group g
   uint32_t unit[MAX_UNITS];       // (group | m-tile << 8 | n-tile << 16), group-major per segment
 };
 
@@ -298,6 +300,15 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
             P.unit[nu++] = (uint32_t)g | ((uint32_t)mt << 8) | ((uint32_t)nt << 16);
     }
     P.unit_off[P.n_seg] = nu;
+    int ic = 0, vc = 0;
+    for (int g = 0; g < P.n_grp; ++g) {
+      P.icum[g] = ic;
+      P.vcum[g] = vc;
+      ic += (TP / 4) * ((P.grp[g].m + 3) >> 2);
+      vc += round4(P.grp[g].m);
+    }
+    P.icum[P.n_grp] = ic;
+    P.vcum[P.n_grp] = vc;
     // members with an exact-order path, decided by rb_initialize (plan_launches)
     // and carried in the device copy of the function record
     P.exact_mem = sizeof(T) == 8 ? (uint32_t)P.fn.reserved & 0xffu : 0u;
@@ -753,18 +764,13 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
   const PlanHead& P = *s.P;
   const int g0 = P.seg[s_first].group0 - P.grp_base;
   const int ng = P.seg[s_end - 1].group0 + P.seg[s_end - 1].n_groups - P.seg[s_first].group0;
-  int total = 0;
-  for (int g = 0; g < ng; ++g) total += (TP / 4) * ((P.grp[g0 + g].m + 3) >> 2);
+  const int i0 = P.icum[g0];
+  const int total = P.icum[g0 + ng] - i0;
   uint32_t nf = 0u;
   for (int t = threadIdx.x; t < total; t += NT) {
-    int g = g0, rem = t, vq = 0;
-    for (;;) {
-      const int cnt = (TP / 4) * ((P.grp[g].m + 3) >> 2);
-      if (rem < cnt) break;
-      rem -= cnt;
-      vq += round4(P.grp[g].m);
-      ++g;
-    }
+    int g = g0;
+    while (P.icum[g + 1] <= i0 + t) ++g;
+    const int rem = i0 + t - P.icum[g], vq = P.vcum[g] - P.vcum[g0];
     const rb_group& G = P.grp[g];
     const float post = (float)P.seg[P.grp_seg[g]].post;
     const int pq = rem % (TP / 4), rq = rem / (TP / 4);
