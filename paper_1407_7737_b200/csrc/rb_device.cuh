@@ -149,6 +149,7 @@ struct PlanHead {
   uint32_t marked;                // fixup_kernel: marked points of the current chunk
   int icum[MAX_GROUPS + 1];       // fp32 rotate: items (4 points x 4 rows) before plan group g
   int vcum[MAX_GROUPS + 1];       // fp32: V rows (4-padded group sizes) before plan group g
+  float gsc32[MAX_GROUPS], gpre32[MAX_GROUPS], gpost32[MAX_GROUPS];  // fp32: group's segment constants
   uint32_t unit[MAX_UNITS];       // (group | m-tile << 8 | n-tile << 16), group-major per segment
 };
 
@@ -306,6 +307,10 @@ __device__ void load_plan(const Args<T>& a, const Smem<T>& s) {
       P.vcum[g] = vc;
       ic += (TP / 4) * ((P.grp[g].m + 3) >> 2);
       vc += round4(P.grp[g].m);
+      const rb_segment& sg = P.seg[P.grp_seg[g]];
+      P.gsc32[g] = (float)sg.scale;
+      P.gpre32[g] = (float)sg.pre;
+      P.gpost32[g] = (float)sg.post;
     }
     P.icum[P.n_grp] = ic;
     P.vcum[P.n_grp] = vc;
@@ -629,8 +634,7 @@ __device__ inline uint32_t gather_v(const Args<float>& a, const Smem<float>& s, 
   uint32_t mx = 0u;
   int vq = 0;
   for (int g = 0; g < ng; ++g) {
-    const rb_segment& sg = P.seg[P.grp_seg[g0 + g]];
-    const float scale = (float)sg.scale, pre = (float)sg.pre;
+    const float scale = P.gsc32[g0 + g], pre = P.gpre32[g0 + g];
     const int kp = round4(P.grp[g0 + g].m);
     const int* qs = s.qsrc + P.gq0[g0 + g];
     const float* qo = s.qo + P.gq0[g0 + g];
@@ -772,7 +776,7 @@ __device__ inline uint32_t rotate(const Args<float>& a, const Smem<float>& s, in
     while (P.icum[g + 1] <= i0 + t) ++g;
     const int rem = i0 + t - P.icum[g], vq = P.vcum[g] - P.vcum[g0];
     const rb_group& G = P.grp[g];
-    const float post = (float)P.seg[P.grp_seg[g]].post;
+    const float post = P.gpost32[g];
     const int pq = rem % (TP / 4), rq = rem / (TP / 4);
     const int m = G.m, m4 = round4(m);
     const int* prow = s.prow + P.gq0[g];
