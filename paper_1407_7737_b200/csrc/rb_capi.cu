@@ -229,6 +229,7 @@ struct rb_engine {
   float* d_v32 = nullptr;
   int* h_flags = nullptr;                    // ring of per-call non-finite flags, mapped
   int* d_flags = nullptr;                    // pinned host memory (device alias of h_flags)
+  int* d_marks = nullptr;                    // device memory, one word per flag slot (Args::mark)
   std::atomic<uint32_t> next_flag{0};
   std::mutex host_mu;                        // host-pointer API pipeline (evaluate_host_locked)
   void* pin_x[2] = {nullptr, nullptr};       // pinned row chunks
@@ -297,6 +298,7 @@ void release(rb_engine* e) {
     if (e->pin_fm[b]) cudaFreeHost(e->pin_fm[b]);
   }
   if (e->h_flags) cudaFreeHost(e->h_flags);
+  cudaFree(e->d_marks);
   if (e->host_stream) cudaStreamDestroy(e->host_stream);
   cudaSetDevice(prev);
   delete e;
@@ -319,6 +321,7 @@ rb::Args<T> make_args(const rb_engine* e, int32_t fn_id, const T* x, int64_t n, 
   a.values = reinterpret_cast<const T*>(pi == 0 ? (const void*)e->d_v64 : (const void*)e->d_v32);
   a.fn = fn_id;
   a.flag = dflag;
+  a.mark = dflag ? e->d_marks + (dflag - e->d_flags) / kSlotInts : nullptr;
   a.ldz = e->ldz[pi];
   a.ldv = L.ldv;
   a.max_q = L.max_q;
@@ -339,7 +342,8 @@ rb_status launch_fixup(rb_engine* e, int32_t fn_id, const double* x, int64_t n, 
   a.nbuf = 1;
   const int64_t nchunks = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(nchunks, e->fixup_grid);
-  void* args[] = {&a};
+  int seq = e->h_flags[(dflag - e->d_flags) + 2];      // the call's sequence number (host memory)
+  void* args[] = {&a, &seq};
   RB_CUDA(cudaLaunchKernel(rb::fixup_f64, dim3(grid), dim3(rb::NT), args, L.smem_nbuf[1], stream));
   g_launches.fetch_add(1);
   return RB_OK;
@@ -1289,6 +1293,10 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   if (s == RB_OK && cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_flags), e->h_flags, 0) !=
                         cudaSuccess)
     s = fail(RB_E_CUDA, "mapped flag pointer failed");
+  // -1: no sequence number (slot seq values start at 0)
+  if (s == RB_OK && (cudaMalloc(reinterpret_cast<void**>(&e->d_marks), sizeof(int) * kFlagSlots) != cudaSuccess ||
+                     cudaMemset(e->d_marks, 0xff, sizeof(int) * kFlagSlots) != cudaSuccess))
+    s = fail(RB_E_CUDA, "mark words allocation failed");
   if (s == RB_OK && cudaStreamCreateWithFlags(&e->host_stream, cudaStreamNonBlocking) != cudaSuccess)
     s = fail(RB_E_CUDA, "stream creation failed");
   cudaSetDevice(prev);
