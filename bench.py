@@ -572,6 +572,7 @@ def run_ours(args):
                        "note": "device: one evaluation of N=1000 rows back to back (CUDA events "
                                "around 8 calls queued together); host: the whole blocking NumPy "
                                "call (validation, H2D, kernel, D2H)"}
+            latency["graph"] = graph_latency(engine, fns[0], precs[0], xrot, stream)
         del xh
 
     # e2e through the public API from pinned host memory (config 5)
@@ -741,6 +742,49 @@ def run_ours(args):
     engine.dispose()
     if world > 1:
         dist.destroy_process_group()
+
+
+def graph_latency(engine, fn, prec, xrot, stream, reps=64, rounds=9):
+    """Config 1 through Engine.capture: the same N=1000 evaluation as CUDA
+    graphs, one per rotating copy of X (so a replay reads X from HBM, not
+    L2, as the timed steps do), replayed back to back -- one cudaGraphLaunch
+    per evaluation, no per-call validation.  Device time per replay (CUDA
+    events around ``reps`` replays on the launching stream) and host time
+    for launch + wait + status of one replay."""
+    import torch
+    caps = [engine.capture(fn, xr[prec], prec) for xr in xrot]
+    for c in caps:
+        c.launch()
+    for c in caps:
+        c.result()
+    dev, host = [], []
+    k = 0
+    for _ in range(rounds):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            caps[k % len(caps)].launch()
+            k += 1
+        e1.record(stream)
+        torch.cuda.synchronize()
+        for c in caps:
+            c.result()
+        dev.append(1e3 * e0.elapsed_time(e1) / reps)
+    for _ in range(reps):
+        c = caps[k % len(caps)]
+        k += 1
+        t0 = time.perf_counter()
+        c.launch().result()
+        host.append(1e6 * (time.perf_counter() - t0))
+    for c in caps:
+        c.close()
+    return {"device_us_per_call_median": statistics.median(dev),
+            "evals_per_s": 1e6 * int(xrot[0][prec].shape[0]) / statistics.median(dev),
+            "host_us_per_call_median": statistics.median(host),
+            "graphs": len(caps),
+            "note": "Engine.capture (rb_graph_capture): one graph per rotating X copy, one "
+                    "cudaGraphLaunch per evaluation; host = launch + wait + status of one replay"}
 
 
 def main():

@@ -204,6 +204,24 @@ rb_status rb_func_evaluate_sharded(rb_sharded* s, int32_t fn_id, int32_t precisi
 rb_status rb_sharded_ticket_status(rb_sharded* s, int32_t device_index, int64_t ticket);
 rb_status rb_dispose_sharded(rb_sharded** s);      /* idempotent; *s = NULL */
 
+/* ---- CUDA graphs -------------------------------------------------------- */
+/* One evaluation captured as a CUDA graph and replayed (no reference
+ * counterpart: the reference has no device; this is the launch-bound
+ * small-batch case of Engine.evaluate, engine.py:174-214, called in a loop
+ * on the same buffers).  rb_graph_capture validates like rb_func_evaluate
+ * and records: reset of the graph's own status words, the evaluation
+ * kernel, and (float64 HappyCat / HGBat functions) the exact-order fixup
+ * pass.  Each rb_graph_launch evaluates the CURRENT contents of d_x into d_f
+ * on `stream`; after the stream has synchronised, rb_graph_status returns
+ * RB_E_NON_FINITE_INPUT if that replay saw a non-finite input.  Replays of
+ * one graph must not overlap (they share the status words). */
+typedef struct rb_graph rb_graph;
+rb_status rb_graph_capture(rb_engine* e, int32_t fn_id, int32_t precision, const void* d_x,
+                           int64_t n, void* d_f, rb_graph** out);
+rb_status rb_graph_launch(rb_graph* g, void* stream);
+rb_status rb_graph_status(rb_graph* g);
+rb_status rb_graph_destroy(rb_graph** g);          /* idempotent; *g = NULL */
+
 /* ---- introspection ---------------------------------------------------- */
 const char* rb_last_error(void);                   /* thread-local message */
 int32_t rb_abi_version(void);

@@ -15,6 +15,7 @@ from .errors import (BatchTooLarge, BenchmarkError, CorruptInstance, DeviceError
                      DimensionMismatch, DimensionTooSmall, DisabledFunction, NonFiniteInput,
                      ParseError, RankDeficiency, UnknownFunction, UnsupportedAtDim2,
                      UseAfterDispose)
-from .engine import Engine, EngineConfig, EvalResult, Pending, PointBatch, initialize
+from .engine import (CapturedEvaluation, Engine, EngineConfig, EvalResult, Pending, PointBatch,
+                     initialize)
 
 __version__ = "0.1.0"

@@ -37,7 +37,8 @@ EXPORTS = ("rb_initialize", "rb_dispose", "rb_func_evaluate", "rb_func_evaluatef
            "rb_debug_phases", "rb_uniform_population", "rb_func_evaluate_async",
            "rb_ticket_status", "rb_initialize_sharded", "rb_func_evaluate_sharded",
            "rb_sharded_ticket_status", "rb_dispose_sharded", "rb_h_func_evaluate_x64",
-           "rb_func_evaluate_many", "rb_h_func_evaluate_many")
+           "rb_func_evaluate_many", "rb_h_func_evaluate_many", "rb_graph_capture",
+           "rb_graph_launch", "rb_graph_status", "rb_graph_destroy")
 RB_DOUBLE, RB_SINGLE = 0, 1
 
 
@@ -104,9 +105,14 @@ def load() -> ctypes.CDLL:
                                              ctypes.POINTER(vp), ctypes.POINTER(i64)]
     lib.rb_sharded_ticket_status.argtypes = [vp, i32, i64]
     lib.rb_dispose_sharded.argtypes = [ctypes.POINTER(vp)]
+    lib.rb_graph_capture.argtypes = [vp, i32, i32, vp, i64, vp, ctypes.POINTER(vp)]
+    lib.rb_graph_launch.argtypes = [vp, vp]
+    lib.rb_graph_status.argtypes = [vp]
+    lib.rb_graph_destroy.argtypes = [ctypes.POINTER(vp)]
     for name in ("rb_func_evaluate_async", "rb_ticket_status", "rb_initialize_sharded",
-                 "rb_func_evaluate_sharded", "rb_sharded_ticket_status", "rb_dispose_sharded", "rb_h_func_evaluate_x64",
-           "rb_func_evaluate_many", "rb_h_func_evaluate_many"):
+                 "rb_func_evaluate_sharded", "rb_sharded_ticket_status", "rb_dispose_sharded",
+                 "rb_h_func_evaluate_x64", "rb_func_evaluate_many", "rb_h_func_evaluate_many",
+                 "rb_graph_capture", "rb_graph_launch", "rb_graph_status", "rb_graph_destroy"):
         getattr(lib, name).restype = i32
     _check_layout(lib)
     _lib = lib

@@ -349,16 +349,9 @@ rb_status launch_fixup(rb_engine* e, int32_t fn_id, const double* x, int64_t n, 
   return RB_OK;
 }
 
-// Validation in the reference's order, then the launch on `stream`; the
-// caller has made e->device current, synchronises and reads the flags
-// (*flag_out: [0] non-finite input, [1] rows marked for the fixup pass).
-// fixup_now: also queue the fixup pass of a float64 exact64 function behind
-// the kernel (callers that do not inspect the flags before using f).
+// Validation in the reference's order (engine.py:180-203).
 template <class T>
-rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
-                      cudaStream_t stream, volatile int** flag_out, bool fixup_now = false,
-                      uint32_t* seq_out = nullptr) {
-  // validation in the reference's order (engine.py:180-203)
+rb_status check_call(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f) {
   if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
   if (fn_id < 0 || fn_id >= (int32_t)e->fns.size())
     return fail(RB_E_UNKNOWN_FUNCTION, "function id " + std::to_string(fn_id) + " is not in 0..36");
@@ -371,6 +364,21 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
   const int pi = sizeof(T) == 8 ? 0 : 1;
   if (!e->why[pi][fn_id].empty())
     return fail(RB_E_UNSUPPORTED, "function " + std::to_string(fn_id) + ": " + e->why[pi][fn_id]);
+  return RB_OK;
+}
+
+// Validation in the reference's order, then the launch on `stream`; the
+// caller has made e->device current, synchronises and reads the flags
+// (*flag_out: [0] non-finite input, [1] rows marked for the fixup pass).
+// fixup_now: also queue the fixup pass of a float64 exact64 function behind
+// the kernel (callers that do not inspect the flags before using f).
+template <class T>
+rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
+                      cudaStream_t stream, volatile int** flag_out, bool fixup_now = false,
+                      uint32_t* seq_out = nullptr) {
+  const rb_status vs = check_call<T>(e, fn_id, x, n, f);
+  if (vs != RB_OK) return vs;
+  const int pi = sizeof(T) == 8 ? 0 : 1;
   const Launch& L = e->launch[pi][fn_id];
 
   const uint32_t seq = e->next_flag.fetch_add(1);
@@ -1220,6 +1228,99 @@ rb_status evaluate_sharded(rb_sharded* sh, int32_t fn_id, const void* const* x_s
   return st;
 }
 
+// ------------------------------------------------------------ CUDA graphs
+// One evaluation (fixed function, precision, device pointers, row count)
+// captured once and replayed: a replay is one cudaGraphLaunch instead of
+// validation + flag bookkeeping + one or two kernel launches, for callers
+// that evaluate the same buffers many times (optimizer loops over small
+// populations, BASELINE config 1).  The graph owns its flag words (mapped
+// host memory, reset by a memset node at the start of every replay) and its
+// device mark word, so replays never touch the engine's call ring.
+struct rb_graph_t {
+  rb_engine* e = nullptr;
+  int device = 0;
+  int* h_flag = nullptr;            // [0] non-finite, [1] rows left for fixup, [2] call number (0)
+  int* d_flag = nullptr;
+  int* d_mark = nullptr;
+  unsigned char* scratch = nullptr; // large-dimension kernel tiles
+  cudaGraphExec_t exec = nullptr;
+};
+
+void release_graph(rb_graph_t* g) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(g->device);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  cudaFree(g->d_mark);
+  cudaFree(g->scratch);
+  if (g->h_flag) cudaFreeHost(g->h_flag);
+  cudaSetDevice(prev);
+  delete g;
+}
+
+template <class T>
+rb_status capture_graph(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f, rb_graph_t** out) {
+  const rb_status vs = check_call<T>(e, fn_id, x, n, f);
+  if (vs != RB_OK) return vs;
+  const int pi = sizeof(T) == 8 ? 0 : 1;
+  const Launch& L = e->launch[pi][fn_id];
+  rb_graph_t* g = new rb_graph_t();
+  g->e = e;
+  g->device = e->device;
+  cudaStream_t cs = nullptr;
+  cudaGraph_t graph = nullptr;
+  rb_status st = RB_OK;
+  auto cuda = [&](cudaError_t err, const char* what) {
+    if (err != cudaSuccess && st == RB_OK)
+      st = fail(RB_E_CUDA, std::string("graph capture: ") + what + ": " + cudaGetErrorString(err));
+    return st == RB_OK;
+  };
+  const int64_t ntiles = (n + rb::TP - 1) / rb::TP;
+  const int grid = (int)std::min<int64_t>(ntiles, L.grid_cap);
+  if (cuda(cudaHostAlloc(reinterpret_cast<void**>(&g->h_flag), kSlotInts * sizeof(int),
+                         cudaHostAllocMapped | cudaHostAllocPortable), "flag") &&
+      cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->d_flag), g->h_flag, 0), "flag pointer") &&
+      cuda(cudaMalloc(reinterpret_cast<void**>(&g->d_mark), sizeof(int)), "mark") &&
+      (!L.big || cuda(cudaMalloc(reinterpret_cast<void**>(&g->scratch), L.per_cta * grid), "scratch")) &&
+      cuda(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream") &&
+      cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin")) {
+    std::memset(g->h_flag, 0, kSlotInts * sizeof(int));
+    rb::Args<T> a = make_args<T>(e, fn_id, x, n, f, nullptr, L);
+    a.flag = g->d_flag;
+    a.mark = g->d_mark;
+    int seq = 0;                    // h_flag[2] after the reset: what mark_fixup copies
+    cuda(cudaMemsetAsync(g->d_flag, 0, kSlotInts * sizeof(int), cs), "flag reset");
+    const bool fixup = sizeof(T) == 8 && e->fixup[fn_id] && !L.big;
+    if (fixup) cuda(cudaMemsetAsync(g->d_mark, 0xff, sizeof(int), cs), "mark reset");
+    if (L.big) {
+      size_t per_cta = L.per_cta;
+      void* args[] = {&a, &g->scratch, &per_cta};
+      cuda(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, cs), "kernel");
+    } else {
+      void* args[] = {&a};
+      cuda(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, cs), "kernel");
+      if (fixup) {
+        rb::Args<T> b = a;
+        b.nbuf = 1;
+        const int fgrid = (int)std::min<int64_t>(ntiles, e->fixup_grid);
+        void* fargs[] = {&b, &seq};
+        cuda(cudaLaunchKernel(rb::fixup_f64, dim3(fgrid), dim3(rb::NT), fargs, L.smem_nbuf[1], cs), "fixup");
+      }
+    }
+    const cudaError_t end = cudaStreamEndCapture(cs, &graph);
+    cuda(end, "end");
+    if (st == RB_OK) cuda(cudaGraphInstantiate(&g->exec, graph, 0), "instantiate");
+  }
+  if (graph) cudaGraphDestroy(graph);
+  if (cs) cudaStreamDestroy(cs);
+  if (st != RB_OK) {
+    release_graph(g);
+    return st;
+  }
+  *out = g;
+  return RB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1531,6 +1632,54 @@ rb_status rb_np_powf(const float* x, const float* y, float* out, int64_t n, void
   g_launches.fetch_add(1);
   RB_CUDA(cudaGetLastError());
   RB_CUDA(cudaStreamSynchronize(st));
+  return RB_OK;
+}
+
+rb_status rb_graph_capture(rb_engine* e, int32_t fn_id, int32_t precision, const void* x, int64_t n,
+                           void* f, rb_graph** out) {
+  NvtxRange range("rb_graph_capture");
+  if (!out) return fail(RB_E_INVALID_ARGUMENT, "null graph handle");
+  *out = nullptr;
+  if (!e) return fail(RB_E_USE_AFTER_DISPOSE, "engine was disposed");
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  if (prev != e->device) RB_CUDA(cudaSetDevice(e->device));
+  rb_graph_t* g = nullptr;
+  rb_status s;
+  if (precision == RB_DOUBLE)
+    s = capture_graph<double>(e, fn_id, static_cast<const double*>(x), n, static_cast<double*>(f), &g);
+  else if (precision == RB_SINGLE)
+    s = capture_graph<float>(e, fn_id, static_cast<const float*>(x), n, static_cast<float*>(f), &g);
+  else
+    s = fail(RB_E_INVALID_ARGUMENT, "precision must be RB_DOUBLE or RB_SINGLE");
+  if (prev != e->device) cudaSetDevice(prev);
+  if (s == RB_OK) *out = reinterpret_cast<rb_graph*>(g);
+  return s;
+}
+
+rb_status rb_graph_launch(rb_graph* graph, void* stream) {
+  rb_graph_t* g = reinterpret_cast<rb_graph_t*>(graph);
+  if (!g) return fail(RB_E_USE_AFTER_DISPOSE, "graph was destroyed");
+  int prev = 0;
+  RB_CUDA(cudaGetDevice(&prev));
+  if (prev != g->device) RB_CUDA(cudaSetDevice(g->device));
+  const cudaError_t err = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+  if (prev != g->device) cudaSetDevice(prev);
+  if (err != cudaSuccess) return fail(RB_E_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(err));
+  g_launches.fetch_add(1);
+  return RB_OK;
+}
+
+rb_status rb_graph_status(rb_graph* graph) {
+  rb_graph_t* g = reinterpret_cast<rb_graph_t*>(graph);
+  if (!g) return fail(RB_E_USE_AFTER_DISPOSE, "graph was destroyed");
+  return reinterpret_cast<volatile int*>(g->h_flag)[0] ? non_finite() : RB_OK;
+}
+
+rb_status rb_graph_destroy(rb_graph** graph) {
+  if (!graph || !*graph) return RB_OK;
+  release_graph(reinterpret_cast<rb_graph_t*>(*graph));
+  *graph = nullptr;
   return RB_OK;
 }
 

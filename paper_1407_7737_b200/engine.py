@@ -215,6 +215,44 @@ class Engine:
         done.record(stream)
         return Pending(out, [(self, ticket.value)], done, keep=(pts,))
 
+    def capture(self, fn_id: int, batch, precision: str | None = None, *,
+                out=None) -> "CapturedEvaluation":
+        """Capture one evaluation of a CUDA-tensor batch as a CUDA graph
+        (rb_graph_capture) for repeated use on the same buffers: each
+        ``launch()`` evaluates the tensor's CURRENT contents with one
+        cudaGraphLaunch, no per-call validation or flag bookkeeping (small
+        populations in an optimizer loop are launch-bound).  Argument
+        errors are raised here, in the reference's order; NonFiniteInput by
+        ``result()`` after each launch."""
+        if self._disposed:
+            raise UseAfterDispose("engine was disposed")
+        if not isinstance(batch, PointBatch):
+            batch = PointBatch(batch)
+        if not _is_torch(batch.data):
+            raise ValueError("capture takes CUDA tensor batches")
+        catalog.lookup(fn_id)
+        fn_id = int(fn_id)
+        if fn_id in self._disabled:
+            raise DisabledFunction(
+                f"function {fn_id} needs dimension >= {catalog.MIN_CONSTRUCTED_DIMENSION}")
+        if batch.count > self.config.max_concurrency:
+            raise BatchTooLarge(f"batch of {batch.count} exceeds "
+                                f"max_concurrency={self.config.max_concurrency}")
+        if batch.dim != self.config.dim:
+            raise DimensionMismatch(f"batch dim {batch.dim} != engine dim {self.config.dim}")
+        precision = precision or self.config.precision
+        if precision not in _DTYPES:
+            raise ValueError(f"precision must be one of {sorted(_DTYPES)}")
+        pts, out = self._device_args(batch.data, precision, out)
+        if pts.data_ptr() != batch.data.data_ptr():
+            raise ValueError("capture needs a contiguous tensor of the evaluation dtype "
+                             "(a converted copy would not see later updates)")
+        handle = ctypes.c_void_p()
+        _lib.check(_lib.load().rb_graph_capture(
+            self._handle, fn_id, _lib.RB_DOUBLE if precision == "double" else _lib.RB_SINGLE,
+            pts.data_ptr(), pts.shape[0], out.data_ptr(), ctypes.byref(handle)))
+        return CapturedEvaluation(self, handle, pts, out)
+
     def evaluate_many(self, calls, batches, *, outs=None) -> "list[Pending]":
         """Several evaluations in ONE native call: ``calls`` = [(fn_id,
         precision), ...].  Host rows (a NumPy array / PointBatch): returns
@@ -360,6 +398,46 @@ class Pending:
             eng.ticket_status(ticket)
         self._keep = ()
         return EvalResult(self.values)
+
+
+class CapturedEvaluation:
+    """An evaluation captured as a CUDA graph (Engine.capture).  ``launch()``
+    queues one replay on the current stream; ``result()`` waits for the
+    latest replay and raises NonFiniteInput if it saw a non-finite input.
+    Replays of one capture must not overlap (they share its status words);
+    the captured tensors are kept alive here."""
+
+    def __init__(self, engine, handle, points, values):
+        self._engine, self._handle, self.points, self.values = engine, handle, points, values
+        self._done = None
+
+    def launch(self) -> "CapturedEvaluation":
+        import torch
+        if self._handle is None or not self._handle.value:
+            raise UseAfterDispose("captured evaluation was closed")
+        stream = torch.cuda.current_stream(self.values.device)
+        _lib.check(_lib.load().rb_graph_launch(self._handle, stream.cuda_stream))
+        if self._done is None:
+            self._done = torch.cuda.Event()
+        self._done.record(stream)
+        return self
+
+    def result(self) -> EvalResult:
+        if self._done is not None:
+            self._done.synchronize()
+        _lib.check(_lib.load().rb_graph_status(self._handle))
+        return EvalResult(self.values)
+
+    def close(self) -> None:
+        if self._handle is not None and self._handle.value:
+            _lib.check(_lib.load().rb_graph_destroy(ctypes.byref(self._handle)))
+        self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class _PointEvaluator:
