@@ -784,7 +784,9 @@ def graph_latency(engine, fn, prec, xrot, stream, reps=64, rounds=9):
             "host_us_per_call_median": statistics.median(host),
             "graphs": len(caps),
             "note": "Engine.capture (rb_graph_capture): one graph per rotating X copy, one "
-                    "cudaGraphLaunch per evaluation; host = launch + wait + status of one replay"}
+                    "cudaGraphLaunch per evaluation, queued back to back (bounded by the host cost "
+                    "of cudaGraphLaunch when it exceeds the 6 us kernel); host = launch + wait + "
+                    "status of one replay"}
 
 
 def main():

@@ -1,7 +1,7 @@
 """One small launch of every kernel family, for compute-sanitizer
 (tools/sanitize.sh): basic (fn 0, 20 with its fixup pass, 8), hybrid-spec
 (24), composition-spec (32, 36), the generic kernel (RB_SPEC=0 run), both
-precisions; the async path, the host pipeline, the sharded P2P-store gather
+precisions; the async path, a captured graph, the host pipeline, the sharded P2P-store gather
 and the on-device population source."""
 import os
 import sys
@@ -25,6 +25,9 @@ for fn in (0, 8, 20, 24, 32, 36):
 xt = torch.from_numpy(x).cuda()
 for p in [eng.evaluate_async(fn, xt, "double") for fn in (20, 33)]:
     p.result()
+cap = eng.capture(20, xt, "double")                 # CUDA graph: reset, kernel, fixup
+cap.launch().result()
+cap.close()
 multi = MultiDeviceEngine(rb.EngineConfig(dim=dim, max_concurrency=256, seed=0), [0, 0])
 multi.evaluate(29, [xt[:35], xt[35:]], "double")
 multi.dispose()
