@@ -240,6 +240,8 @@ struct rb_engine {
   cudaStream_t copy_stream = nullptr;        // H2D of row chunks
   cudaStream_t d2h_stream = nullptr;         // many-call path: D2H of a chunk's values
   cudaEvent_t computed[2] = {nullptr, nullptr};
+  cudaStream_t many_stream2 = nullptr;       // many-call path: every other call of a chunk
+  cudaEvent_t computed2[2] = {nullptr, nullptr}, ready2 = nullptr;
   cudaEvent_t x_ready[2] = {nullptr, nullptr}, f_ready[2] = {nullptr, nullptr};
   float* dev_x32 = nullptr;                  // many-call host path: the float32 rows of a chunk
   void* pin_xm[2] = {nullptr, nullptr};      // ... its (larger) row chunks
@@ -288,6 +290,10 @@ void release(rb_engine* e) {
   if (e->d2h_stream) cudaStreamDestroy(e->d2h_stream);
   for (int b = 0; b < 2; ++b)
     if (e->computed[b]) cudaEventDestroy(e->computed[b]);
+  if (e->many_stream2) cudaStreamDestroy(e->many_stream2);
+  for (int b = 0; b < 2; ++b)
+    if (e->computed2[b]) cudaEventDestroy(e->computed2[b]);
+  if (e->ready2) cudaEventDestroy(e->ready2);
   cudaFree(e->dev_x32);
   for (int b = 0; b < 2; ++b) {
     cudaFree(e->dev_xm[b]);
@@ -567,6 +573,9 @@ rb_status ensure_pipeline(rb_engine* e) {
   RB_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
   RB_CUDA(cudaStreamCreateWithFlags(&e->d2h_stream, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) RB_CUDA(cudaEventCreateWithFlags(&e->computed[b], cudaEventDisableTiming));
+  RB_CUDA(cudaStreamCreateWithFlags(&e->many_stream2, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) RB_CUDA(cudaEventCreateWithFlags(&e->computed2[b], cudaEventDisableTiming));
+  RB_CUDA(cudaEventCreateWithFlags(&e->ready2, cudaEventDisableTiming));
   e->chunk_rows = rows;
   return RB_OK;
 }
@@ -754,6 +763,12 @@ rb_status evaluate_host_many_locked(rb_engine* e, int32_t n_calls, const int32_t
       break;
     }
     const double* x64 = static_cast<const double*>(e->dev_xm[b]);
+    // dev_x32 is single-buffered: the previous chunk's calls on the second
+    // stream read it until they finish
+    if (c >= 1 && cudaStreamWaitEvent(e->host_stream, e->computed2[b ^ 1], 0) != cudaSuccess) {
+      st = fail(RB_E_CUDA, "host pipeline: event wait failed");
+      break;
+    }
     if (any32) {
       const int grid = (int)std::min<int64_t>((rows * dim + 255) / 256, 148 * 8);
       rb::cast_rows_kernel<<<grid, 256, 0, e->host_stream>>>(x64, e->dev_x32, rows * dim);
@@ -764,20 +779,30 @@ rb_status evaluate_host_many_locked(rb_engine* e, int32_t n_calls, const int32_t
       st = fail(RB_E_CUDA, "host pipeline: event wait failed");   // dev_fm[b] copied out
       break;
     }
+    // the calls alternate between two streams, so one kernel's last wave
+    // (a chunk is ~10 waves per launch) overlaps the next kernel's first
+    if (cudaEventRecord(e->ready2, e->host_stream) != cudaSuccess ||
+        cudaStreamWaitEvent(e->many_stream2, e->ready2, 0) != cudaSuccess) {
+      st = fail(RB_E_CUDA, "host pipeline: event wait failed");
+      break;
+    }
     for (int32_t i = 0; i < n_calls && st == RB_OK; ++i) {
       volatile int* flag = nullptr;
       void* fi = fb + sizeof(double) * cap * i;
+      cudaStream_t cs = (i & 1) ? e->many_stream2 : e->host_stream;
       if (precisions[i] == RB_DOUBLE)
-        st = launch_eval<double>(e, fn_ids[i], x64, rows, static_cast<double*>(fi), e->host_stream, &flag, true);
+        st = launch_eval<double>(e, fn_ids[i], x64, rows, static_cast<double*>(fi), cs, &flag, true);
       else
-        st = launch_eval<float>(e, fn_ids[i], e->dev_x32, rows, static_cast<float*>(fi), e->host_stream, &flag, true);
+        st = launch_eval<float>(e, fn_ids[i], e->dev_x32, rows, static_cast<float*>(fi), cs, &flag, true);
       if (st == RB_OK) flags.push_back(flag);
     }
     if (st != RB_OK) break;
     // the values leave on their own stream (PCIe is full duplex), so chunk
     // c+1's kernels start as soon as chunk c's are done
     if (cudaEventRecord(e->computed[b], e->host_stream) != cudaSuccess ||
+        cudaEventRecord(e->computed2[b], e->many_stream2) != cudaSuccess ||
         cudaStreamWaitEvent(e->d2h_stream, e->computed[b], 0) != cudaSuccess ||
+        cudaStreamWaitEvent(e->d2h_stream, e->computed2[b], 0) != cudaSuccess ||
         cudaMemcpyAsync(e->pin_fm[b], e->dev_fm[b], sizeof(double) * cap * n_calls, cudaMemcpyDeviceToHost,
                         e->d2h_stream) != cudaSuccess ||
         cudaEventRecord(e->f_ready[b], e->d2h_stream) != cudaSuccess)
@@ -786,6 +811,7 @@ rb_status evaluate_host_many_locked(rb_engine* e, int32_t n_calls, const int32_t
   if (st == RB_OK)
     for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks && st == RB_OK; ++c) st = drain(c);
   cudaStreamSynchronize(e->host_stream);
+  cudaStreamSynchronize(e->many_stream2);
   cudaStreamSynchronize(e->copy_stream);
   cudaStreamSynchronize(e->d2h_stream);
   if (st != RB_OK) return st;
