@@ -416,12 +416,16 @@ def run_ours(args):
     # N > 1 GPUs: per-call submits, each with its fitness all-gather
     calls = [(fn, p) for p in precs for fn in fns]
     out_bufs = {p: local_bufs[p][0] for p in precs}
+    # every call keeps its own values (distinct outputs also let the engine
+    # overlap consecutive calls on two streams, rb_func_evaluate_many)
+    call_outs = ([torch.empty(shard.count, dtype=dts[p], device=dev) for _, p in calls]
+                 if world == 1 else None)
 
     def step_many():
         k0 = step.calls
         step.calls += len(calls)
         return engine.evaluate_many(calls, [xrot[(k0 + i) % n_rot][p] for i, (fn, p) in enumerate(calls)],
-                                    outs=[out_bufs[p] for _, p in calls])
+                                    outs=call_outs)
 
     timed_step = step_many if world == 1 else (lambda: step(False))
     for _ in range(args.warmup):

@@ -6,7 +6,8 @@ Prints, per path, microseconds per evaluation:
   enqueue_async   host time to queue one evaluate_async call (Python + native)
   enqueue_native  host time per call inside ONE rb_func_evaluate_many of K calls
   device_async    device time per call, K async calls queued (CUDA events)
-  device_many     device time per call, K calls in one native call
+  device_many     device time per call, K calls in one native call (one output)
+  device_many_distinct  the same with a distinct output per call (two streams)
   blocking_dev    Engine.evaluate on a CUDA tensor (blocking, status read)
   blocking_numpy  Engine.evaluate on a NumPy array (H2D + kernel + D2H)
 Run the same command under ncu (--metrics gpu__time_duration.sum) for the
@@ -66,6 +67,9 @@ def main():
         lambda: [eng.evaluate_async(fn, xd, p, out=out) for _ in range(K)])
     res["enqueue_native_us"], res["device_many_us"] = timed(
         lambda: eng.evaluate_many([(fn, p)] * K, [xd] * K, outs=[out] * K))
+    outs = [torch.empty_like(out) for _ in range(K)]      # distinct outputs: two streams
+    res["enqueue_native_distinct_us"], res["device_many_distinct_us"] = timed(
+        lambda: eng.evaluate_many([(fn, p)] * K, [xd] * K, outs=outs))
 
     for name, x in (("blocking_dev_us", xd), ("blocking_numpy_us", xh)):
         ts = []
