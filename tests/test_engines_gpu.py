@@ -170,3 +170,29 @@ def test_two_engines_from_threads_share_the_staging_pool():
             assert np.array_equal(a, b)
     for e in engs:
         e.dispose()
+
+
+def test_many_call_fork_keeps_stream_order_and_values():
+    # rb_func_evaluate_many runs short calls with disjoint outputs on two
+    # streams (forked from the caller's and joined back): the values equal
+    # one call at a time, and work queued after it on the caller's stream
+    # sees every value; overlapping outputs keep one stream (last call wins)
+    import torch
+    dim, n = 30, 5000
+    eng = rb.initialize(rb.EngineConfig(dim=dim, max_concurrency=n, seed=1))
+    x = torch.from_numpy(population(dim, n, seed=11)).cuda()
+    x32 = x.float()
+    calls = [(fn, p) for p in ("double", "single") for fn in eng.enabled_ids]
+    batches = {"double": x, "single": x32}
+    outs = [torch.full((n,), float("nan"), dtype=batches[p].dtype, device="cuda") for _, p in calls]
+    eng.evaluate_many(calls, batches, outs=outs)
+    sums = torch.stack([o.double().sum() for o in outs])          # queued behind the join
+    for (fn, p), o in zip(calls, outs):
+        want = eng.evaluate(fn, batches[p], p).values
+        assert torch.equal(o, want), (fn, p)
+    assert torch.isfinite(sums).all()
+    shared = torch.empty(n, dtype=torch.float64, device="cuda")
+    pend = eng.evaluate_many([(0, "double"), (8, "double"), (29, "double")], x, outs=[shared] * 3)
+    pend[-1].result()
+    assert torch.equal(shared, eng.evaluate(29, x, "double").values)
+    eng.dispose()
