@@ -22,7 +22,7 @@ for c in range(1, 6):
     if not lines:
         continue
     d = json.loads(lines[-1])
-    rec = {k: d.get(k) for k in ("config", "value", "unit", "ms_per_step", "dtype", "e2e", "e2e_numpy",
+    rec = {k: d.get(k) for k in ("config", "value", "unit", "ms_per_step", "dtype", "e2e", "e2e_pinned_tensor", "e2e_numpy",
                                  "latency", "cpu_baseline", "clocks", "per_precision_evals_per_s")}
     rec["roofline"] = {k: d["roofline"].get(k) for k in ("bound", "achieved", "peak", "unit", "frac",
                                                           "kernel", "suite_frac", "peak_source")}
