@@ -214,7 +214,9 @@ rb_status rb_dispose_sharded(rb_sharded** s);      /* idempotent; *s = NULL */
  * pass.  Each rb_graph_launch evaluates the CURRENT contents of d_x into d_f
  * on `stream`; after the stream has synchronised, rb_graph_status returns
  * RB_E_NON_FINITE_INPUT if that replay saw a non-finite input.  Replays of
- * one graph must not overlap (they share the status words). */
+ * one graph must not overlap (they share the status words).  A graph reads
+ * its engine's device tables: destroy it before rb_dispose of the engine
+ * (Engine.dispose closes its captures). */
 typedef struct rb_graph rb_graph;
 rb_status rb_graph_capture(rb_engine* e, int32_t fn_id, int32_t precision, const void* d_x,
                            int64_t n, void* d_f, rb_graph** out);

@@ -708,7 +708,11 @@ rb_status evaluate_host_many_locked(rb_engine* e, int32_t n_calls, const int32_t
   // 343, 64 MB 446, 128 MB 507, 256 MB 548 M evals/s; 128 MB keeps the
   // pinned staging under ~0.5 GB)
   if (!e->many_rows) {
-    const int64_t rows = std::max<int64_t>(1, (int64_t)((size_t(128) << 20) / (sizeof(double) * dim)));
+    static const size_t many_bytes = [] {     // RB_MANY_CHUNK_MB (default 128)
+      const char* v = std::getenv("RB_MANY_CHUNK_MB");
+      return (v ? size_t(std::max(1, std::atoi(v))) : size_t(128)) << 20;
+    }();
+    const int64_t rows = std::max<int64_t>(1, (int64_t)(many_bytes / (sizeof(double) * dim)));
     for (int b = 0; b < 2; ++b) {
       RB_CUDA(cudaMallocHost(&e->pin_xm[b], sizeof(double) * rows * dim));
       RB_CUDA(cudaMalloc(&e->dev_xm[b], sizeof(double) * rows * dim));

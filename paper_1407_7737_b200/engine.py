@@ -125,6 +125,8 @@ class Engine:
                                      int(config.max_concurrency), int(config.device),
                                      ctypes.byref(handle)))
         self._handle = handle
+        import weakref
+        self._captures = weakref.WeakSet()      # graphs reference the device pack: closed by dispose()
         # engine.py:155-159 keeps one per-point evaluator per (fn, precision);
         # here each is a handle onto the device-resident instance
         self._evaluators = {(fn, prec): _PointEvaluator(self, fn, prec)
@@ -251,7 +253,9 @@ class Engine:
         _lib.check(_lib.load().rb_graph_capture(
             self._handle, fn_id, _lib.RB_DOUBLE if precision == "double" else _lib.RB_SINGLE,
             pts.data_ptr(), pts.shape[0], out.data_ptr(), ctypes.byref(handle)))
-        return CapturedEvaluation(self, handle, pts, out)
+        cap = CapturedEvaluation(self, handle, pts, out)
+        self._captures.add(cap)
+        return cap
 
     def evaluate_many(self, calls, batches, *, outs=None) -> "list[Pending]":
         """Several evaluations in ONE native call: ``calls`` = [(fn_id,
@@ -332,6 +336,8 @@ class Engine:
     def dispose(self) -> None:
         """Free the device pack; a second dispose is a no-op (engine.py:219-222)."""
         if not self._disposed:
+            for cap in list(getattr(self, "_captures", ())):
+                cap.close()
             _lib.check(_lib.load().rb_dispose(ctypes.byref(self._handle)))
             self._pack = None
             self._evaluators = None

@@ -111,3 +111,14 @@ def test_large_dimension_kernel_captures(monkeypatch):
             assert _same(cap.launch().result().values, big.evaluate(fn, xs, prec).values), (fn, prec)
         cap.close()
     big.dispose()
+
+
+def test_dispose_closes_captures():
+    import torch
+    eng = rb.initialize(rb.EngineConfig(dim=10, max_concurrency=64, seed=0))
+    x = torch.zeros((8, 10), dtype=torch.float64, device="cuda")
+    cap = eng.capture(0, x)
+    cap.launch().result()
+    eng.dispose()
+    with pytest.raises(rb.UseAfterDispose):
+        cap.launch()
