@@ -354,8 +354,7 @@ rb_status launch_fixup(rb_engine* e, int32_t fn_id, const double* x, int64_t n, 
   a.nbuf = 1;
   const int64_t nchunks = (n + rb::TP - 1) / rb::TP;
   const int grid = (int)std::min<int64_t>(nchunks, e->fixup_grid);
-  int seq = e->h_flags[(dflag - e->d_flags) + 2];      // the call's sequence number (host memory)
-  void* args[] = {&a, &seq};
+  void* args[] = {&a};
   RB_CUDA(cudaLaunchKernel(rb::fixup_f64, dim3(grid), dim3(rb::NT), args, L.smem_nbuf[1], stream));
   g_launches.fetch_add(1);
   return RB_OK;
@@ -423,6 +422,8 @@ rb_status launch_eval(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f,
     return RB_OK;
   }
   void* args[] = {&a};
+  if (sizeof(T) == 8 && e->fixup[fn_id])   // the kernel may mark rows: a clean word for this call
+    RB_CUDA(cudaMemsetAsync(a.mark, 0, sizeof(int), stream));
   RB_CUDA(cudaLaunchKernel(L.func, dim3(grid), dim3(rb::NT), args, L.smem, stream));
   g_launches.fetch_add(1);
   if constexpr (sizeof(T) == 8) {
@@ -1324,10 +1325,9 @@ rb_status capture_graph(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f
     rb::Args<T> a = make_args<T>(e, fn_id, x, n, f, nullptr, L);
     a.flag = g->d_flag;
     a.mark = g->d_mark;
-    int seq = 0;                    // h_flag[2] after the reset: what mark_fixup copies
     cuda(cudaMemsetAsync(g->d_flag, 0, kSlotInts * sizeof(int), cs), "flag reset");
     const bool fixup = sizeof(T) == 8 && e->fixup[fn_id] && !L.big;
-    if (fixup) cuda(cudaMemsetAsync(g->d_mark, 0xff, sizeof(int), cs), "mark reset");
+    if (fixup) cuda(cudaMemsetAsync(g->d_mark, 0, sizeof(int), cs), "mark reset");
     if (L.big) {
       size_t per_cta = L.per_cta;
       void* args[] = {&a, &g->scratch, &per_cta};
@@ -1339,7 +1339,7 @@ rb_status capture_graph(rb_engine* e, int32_t fn_id, const T* x, int64_t n, T* f
         rb::Args<T> b = a;
         b.nbuf = 1;
         const int fgrid = (int)std::min<int64_t>(ntiles, e->fixup_grid);
-        void* fargs[] = {&b, &seq};
+        void* fargs[] = {&b};
         cuda(cudaLaunchKernel(rb::fixup_f64, dim3(fgrid), dim3(rb::NT), fargs, L.smem_nbuf[1], cs), "fixup");
       }
     }
@@ -1430,9 +1430,8 @@ rb_status rb_initialize(const rb_pack* pk, int64_t max_concurrency, int32_t devi
   if (s == RB_OK && cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_flags), e->h_flags, 0) !=
                         cudaSuccess)
     s = fail(RB_E_CUDA, "mapped flag pointer failed");
-  // -1: no sequence number (slot seq values start at 0)
   if (s == RB_OK && (cudaMalloc(reinterpret_cast<void**>(&e->d_marks), sizeof(int) * kFlagSlots) != cudaSuccess ||
-                     cudaMemset(e->d_marks, 0xff, sizeof(int) * kFlagSlots) != cudaSuccess))
+                     cudaMemset(e->d_marks, 0, sizeof(int) * kFlagSlots) != cudaSuccess))
     s = fail(RB_E_CUDA, "mark words allocation failed");
   if (s == RB_OK && cudaStreamCreateWithFlags(&e->host_stream, cudaStreamNonBlocking) != cudaSuccess)
     s = fail(RB_E_CUDA, "stream creation failed");
