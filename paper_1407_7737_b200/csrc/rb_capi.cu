@@ -867,7 +867,7 @@ rb_status plan_launches(rb_engine* e, const rb_pack* pk, int device) {
     e->why[pi].assign(nf, std::string());
   }
   e->fixup.assign(nf, 0);
-  e->fixup_grid = sms;
+  e->fixup_grid = sms * RB_FIXUP_BLOCKS;
   std::map<const void*, size_t> need;       // dynamic shared memory per kernel
   std::vector<int> variant(nf, rb::N_VARIANTS - 1);
   std::vector<int> spec(nf, -1);            // function-specialised kernel (rb_fnspec.cuh)
