@@ -177,7 +177,12 @@ rb_status rb_ticket_status(rb_engine* e, int64_t ticket);
 /* n_calls stream-ordered evaluations in one call (e.g. every function of the
  * suite on one population): call i is rb_func_evaluate_async(e, fn_ids[i],
  * precisions[i], x[i], n[i], f[i], stream, &tickets[i]).  Stops at the first
- * argument error (its status is returned; later tickets are not written). */
+ * argument error (its status is returned; later tickets are not written).
+ * When every f[i] is disjoint from the other outputs and from every input,
+ * and each call is at most RB_FORK_WAVES (default 128) waves of the grid,
+ * the calls alternate between `stream` and an engine stream forked from it
+ * and joined back before returning: work queued on `stream` afterwards
+ * still sees every value. */
 rb_status rb_func_evaluate_many(rb_engine* e, int32_t n_calls, const int32_t* fn_ids,
                                 const int32_t* precisions, const void* const* x, const int64_t* n,
                                 void* const* f, void* stream, int64_t* tickets);
