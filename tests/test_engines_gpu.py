@@ -195,4 +195,15 @@ def test_many_call_fork_keeps_stream_order_and_values():
     pend = eng.evaluate_many([(0, "double"), (8, "double"), (29, "double")], x, outs=[shared] * 3)
     pend[-1].result()
     assert torch.equal(shared, eng.evaluate(29, x, "double").values)
+    # an output inside a later call's input: not forked, calls stay in order
+    # (call 0 writes column 0 of the buffer call 1 then reads)
+    buf = x.clone()
+    col0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    ref = eng.evaluate(3, x, "double").values
+    ins = [x, buf]
+    outs2 = [buf.view(-1)[:n], col0]
+    eng.evaluate_many([(3, "double"), (0, "double")], ins, outs=outs2)[1].result()
+    after = x.clone().view(-1)
+    after[:n] = ref
+    assert torch.equal(col0, eng.evaluate(0, after.view(n, dim), "double").values)
     eng.dispose()
