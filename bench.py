@@ -334,13 +334,22 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RB_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0, gloo
+    # collectives -- runs the multi-rank code path on a one-GPU box; its
+    # numbers are not a scaling measurement
+    share = os.environ.get("RB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if local >= torch.cuda.device_count():
         raise SystemExit(f"rank {rank}: --gpus {world} needs {world} GPUs, "
                          f"{torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:

@@ -144,3 +144,24 @@ def test_evaluate_many_matches_single_calls():
     with pytest.raises(rb.UnknownFunction):
         eng.evaluate_many([(40, "double")], xt)
     eng.dispose()
+
+
+def test_bench_multi_rank_path_runs_on_one_gpu():
+    # bench.py --gpus 2 as the driver launches it (torchrun, 127.0.0.1), with
+    # both ranks on cuda:0 and gloo collectives (RB_BENCH_SHARE_GPU=1): the
+    # sharded step, the all-gather, the e2e step and max-over-ranks timing
+    # all run; rank 0 prints one JSON line for 2 GPUs
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, RB_BENCH_SHARE_GPU="1")
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--rows", "20000", "--steps", "3",
+                          "--warmup", "3", "--fns", "0,8,20,29", "--no-cpu"],
+                         capture_output=True, text=True, env=env, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"] == "rows/2"
