@@ -524,11 +524,15 @@ __device__ __forceinline__ void dmma_epilogue(const Args<double>& a, const Smem<
 
 // Both m-tiles of the tile (MT2): each B fragment load feeds 2 x R
 // DMMAs (the two 16-point m-tiles), halving the B traffic from L1 / L2.
+#ifndef RB_DMMA_UNROLL_MT2
+#define RB_DMMA_UNROLL_MT2 3            // A/B: 2 -> 3 +3 % on float64 basic functions, 4 no better
+#endif
+constexpr int kDmmaUnrollMt2 = RB_DMMA_UNROLL_MT2;
 template <int R>
 __device__ __forceinline__ void dmma_run_mt2(const double* X0, const double* X1, const double* X2,
                                              const double* X3, const int* qs, const double* qo,
                                              const double* F, int nks, double (&acc)[2][2][4]) {
-#pragma unroll 2
+#pragma unroll kDmmaUnrollMt2
   for (int ks = 0; ks < nks; ++ks) {
     const int col = qs[ks * 4];
     const double o = qo[ks * 4];

@@ -1,0 +1,14 @@
+# A/B of DMMA unroll variants: per-precision suite rate and fp64 basic / composition rates
+for v in base m3 m4 u2 base; do
+  RB_LIB=paper_1407_7737_b200/variants/lib_$v.so timeout 600 python bench.py --rows 10000000 --steps 2 --warmup 3 --no-cpu --no-e2e --breakdown gpurun_out/abu_$v.json > gpurun_out/abu_$v.txt 2>/dev/null
+  python - $v <<'PY'
+import json, sys
+v = sys.argv[1]
+d = json.load(open(f"gpurun_out/abu_{v}.json"))
+r = {(x["fn"], x["precision"]): x["evals_per_s"] / 1e6 for x in d["rows"]}
+l = [x for x in open(f"gpurun_out/abu_{v}.txt") if x.startswith("{")][-1]
+j = json.loads(l)
+print(v, "suite", round(j["value"] / 1e6, 1), "f64", round(j["per_precision_evals_per_s"]["double"] / 1e6, 1),
+      "basic f64", [round(r[(f, "double")]) for f in (0, 4, 9, 20, 24)], "comp f64", [round(r[(f, "double")]) for f in (29, 32, 35)])
+PY
+done
